@@ -1,0 +1,4 @@
+// Reference include path (/root/reference/proj/include/mdgemm/dispatch.hpp);
+// the B200 build declares everything in one header.
+#pragma once
+#include "mdgemm/mdgemm.hpp"

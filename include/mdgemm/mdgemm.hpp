@@ -1,0 +1,293 @@
+// mdgemm.hpp -- C++ API of the B200-native mixed-datatype gemm.
+//
+// Source-compatible with the reference engine's public headers
+// (/root/reference/proj/include/mdgemm/{dtypes,kernels,packing,config,
+// dispatch,case_label}.hpp): the same namespace, type names, enumerators,
+// member names and function signatures, so code written against the
+// reference recompiles unchanged.  What differs is underneath: MatrixView
+// bases may be device pointers (or host pointers, which gemm() stages through
+// HBM), and gemm() executes on an sm_100a GPU through the C ABI in
+// include/mdgemm_b200.h.  The per-file forwarding headers in this directory
+// keep the reference's include paths working.
+#pragma once
+
+#include <complex>
+#include <cstddef>
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace mdgemm {
+
+// ------------------------------------------------------------------ errors
+// dtypes.hpp:14-20.  ScalarPolicyError marks an alpha the case cannot honor.
+struct Error : std::runtime_error {
+  explicit Error(const std::string& what) : std::runtime_error(what) {}
+};
+struct ScalarPolicyError : Error {
+  explicit ScalarPolicyError(const std::string& what) : Error(what) {}
+};
+
+// --------------------------------------------------------------- datatypes
+enum class Domain : std::uint8_t { Real, Complex };
+enum class Precision : std::uint8_t { Single, Double };
+
+// Unit roundoff 2^-24 / 2^-53 (dtypes.hpp:25-28).
+constexpr double eps_of(Precision p) { return p == Precision::Double ? 0x1p-53 : 0x1p-24; }
+constexpr std::size_t real_size(Precision p) { return p == Precision::Double ? 8u : 4u; }
+
+struct Datatype {
+  Domain domain = Domain::Real;
+  Precision precision = Precision::Double;
+  friend constexpr bool operator==(Datatype x, Datatype y) {
+    return x.domain == y.domain && x.precision == y.precision;
+  }
+  friend constexpr bool operator!=(Datatype x, Datatype y) { return !(x == y); }
+};
+
+inline constexpr Datatype dt_s{Domain::Real, Precision::Single};
+inline constexpr Datatype dt_d{Domain::Real, Precision::Double};
+inline constexpr Datatype dt_c{Domain::Complex, Precision::Single};
+inline constexpr Datatype dt_z{Domain::Complex, Precision::Double};
+
+constexpr std::size_t dtype_size(Datatype t) {
+  return (t.domain == Domain::Complex ? 2u : 1u) * real_size(t.precision);
+}
+
+char dtype_letter(Datatype t);
+Datatype dtype_from_letter(char ch);
+char precision_letter(Precision p);
+Precision precision_from_letter(char ch);
+std::string to_string(Datatype t);
+
+enum class CaseId : std::uint8_t { C0, C1a, C1b, C1c, C2ab, C2ac, C2bc, C3 };
+const char* to_string(CaseId c);
+
+// ------------------------------------------------------------------ scalars
+// Payload in double, exactly representable in the scalar's precision.
+struct Scalar {
+  double re = 0.0;
+  double im = 0.0;
+  Datatype dtype = dt_d;
+
+  bool is_real() const { return dtype.domain == Domain::Real; }
+  bool is_zero() const { return re == 0.0 && im == 0.0; }
+  bool is_one() const { return re == 1.0 && im == 0.0; }
+  std::complex<double> value() const { return {re, im}; }
+
+  static Scalar real_value(double v, Precision p = Precision::Double);
+  static Scalar complex_value(double r, double i, Precision p = Precision::Double);
+};
+
+Scalar typecast_scalar(Scalar s, Datatype target);
+Scalar project_scalar(Scalar s, Precision p);
+
+// ------------------------------------------------------------------- views
+enum class Part : std::uint8_t { Re, Im };
+enum class FlattenAxis : std::uint8_t { Rows, Cols };
+enum class StorageKind : std::uint8_t { ColumnStored, RowStored, GeneralStored };
+
+struct MatrixView {
+  std::byte* base = nullptr;
+  std::int64_t m = 0;
+  std::int64_t n = 0;
+  std::int64_t rs = 0;
+  std::int64_t cs = 0;
+  Datatype dtype = dt_d;
+  bool conj = false;
+  Precision comp_prec = Precision::Double;
+  Datatype target_dtype = dt_d;
+
+  static MatrixView make(void* base, std::int64_t m, std::int64_t n, std::int64_t rs,
+                         std::int64_t cs, Datatype dtype);
+
+  std::byte* elem_ptr(std::int64_t i, std::int64_t j) const {
+    return base + static_cast<std::size_t>(i * rs + j * cs) * dtype_size(dtype);
+  }
+  MatrixView with_conj(bool c) const {
+    MatrixView v = *this;
+    v.conj = c;
+    return v;
+  }
+  MatrixView with_comp_prec(Precision p) const {
+    MatrixView v = *this;
+    v.comp_prec = p;
+    return v;
+  }
+};
+
+MatrixView induced_transpose(MatrixView v);
+MatrixView real_projection(MatrixView v, Part part);
+bool can_flatten(const MatrixView& v, FlattenAxis axis);
+MatrixView real_flatten(MatrixView v, FlattenAxis axis);
+MatrixView slice(MatrixView v, std::int64_t i0, std::int64_t j0, std::int64_t mm,
+                 std::int64_t nn);
+StorageKind storage_kind(const MatrixView& v);
+
+// Host-memory element access (the views must hold host pointers).
+std::complex<double> load_elem(const MatrixView& v, std::int64_t i, std::int64_t j);
+void store_elem(const MatrixView& v, std::int64_t i, std::int64_t j, std::complex<double> value);
+
+std::pair<const std::byte*, const std::byte*> byte_range(const MatrixView& v);
+bool ranges_overlap(const MatrixView& a, const MatrixView& b);
+
+// ------------------------------------------------------ microkernel metadata
+enum class Preference : std::uint8_t { Column, Row };
+enum class PairAxis : std::uint8_t { None, Rows, Cols };
+enum class OneMVariant : std::uint8_t { Column, Row };
+
+struct UkrDescriptor {
+  Precision precision = Precision::Double;
+  int mr = 4;
+  int nr = 4;
+  Preference preference = Preference::Column;
+};
+
+inline constexpr int kMaxUkrDim = 32;
+
+class FlopCounter {
+ public:
+  void add(std::uint64_t n) { flops_ += n; }
+  void merge(const FlopCounter& other) { flops_ += other.flops_; }
+  void reset() { flops_ = 0; }
+  std::uint64_t value() const { return flops_; }
+
+ private:
+  std::uint64_t flops_ = 0;
+};
+
+// ------------------------------------------------------------------ packing
+enum class PackFormat : std::uint8_t { Standard, OneE, OneR };
+enum class Side : std::uint8_t { Left, Right };
+
+// Bytes of the packed block (packing.hpp:101-102).
+std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Datatype target,
+                         std::int64_t reg_block);
+
+// Device pack: typecast/conj/scale/format `src` (device memory) into `dst`
+// (device memory, packed_bytes() long) in the reference's panel layout.
+// B200 counterpart of pack_block_into (packing.hpp:118-120).
+void pack_block_device(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
+                       Scalar scale, Datatype target, std::int64_t reg_block,
+                       void* stream = nullptr);
+
+// ------------------------------------------------------------------- config
+struct BlockingParams {
+  std::int64_t mc = 0;
+  std::int64_t nc = 0;
+  std::int64_t kc = 0;
+  int mr = 0;
+  int nr = 0;
+  int threads = 1;
+};
+
+enum class CTempMode : std::uint8_t { Auto, On, Off };
+
+// B200 extension: which device arithmetic gemm() uses (see mdgemm_b200.h).
+enum class Numerics : std::uint8_t { Fast, Exact };
+
+struct Config {
+  BlockingParams single_params{128, 1024, 256, 8, 8, 1};
+  BlockingParams double_params{64, 512, 128, 4, 4, 1};
+  int threads = 1;
+  Preference preference = Preference::Column;
+  CTempMode ctemp = CTempMode::Auto;
+  Numerics numerics = Numerics::Fast;
+
+  static Config defaults() { return Config{}; }
+  static Config load(const std::optional<std::string>& file = std::nullopt, bool apply_env = true);
+  void set(const std::string& key, const std::string& value);
+  void validate() const;
+
+  BlockingParams blocking(Precision p) const {
+    BlockingParams bp = p == Precision::Double ? double_params : single_params;
+    bp.threads = threads;
+    return bp;
+  }
+  UkrDescriptor ukr(Precision p) const {
+    const BlockingParams& bp = p == Precision::Double ? double_params : single_params;
+    return UkrDescriptor{p, bp.mr, bp.nr, preference};
+  }
+  std::string describe() const;
+};
+
+// ----------------------------------------------------------------- dispatch
+CaseId classify_case(Domain c, Domain a, Domain b);
+Precision resolve_comp_precision(const MatrixView& c);
+std::uint64_t flops_of_case(CaseId case_id, std::int64_t m, std::int64_t n, std::int64_t k);
+std::pair<Scalar, Scalar> apply_scalar_policy(Scalar alpha, Scalar beta, CaseId case_id,
+                                              Precision comp_prec, Precision c_storage_prec);
+
+enum class UkrPath : std::uint8_t { Direct, Temp, OneMColumn, OneMRow };
+enum class MacroMode : std::uint8_t { Standard, AccumulateTypecast };
+
+struct CTempDescriptor {
+  std::int64_t rows = 0;
+  std::int64_t cols = 0;
+  Precision precision = Precision::Double;
+  enum class Mode : std::uint8_t { CopyBack, AccumulateBack } mode = Mode::AccumulateBack;
+};
+
+struct ExecutionPlan {
+  CaseId case_id = CaseId::C0;
+  bool logical_transpose = false;
+  Precision comp_prec = Precision::Double;
+  std::int64_t m = 0, n = 0, k = 0;
+
+  MatrixView a, b, c;
+  PackFormat format_a = PackFormat::Standard;
+  PackFormat format_b = PackFormat::Standard;
+  bool conj_a = false;
+  bool conj_b = false;
+  Datatype target_dtype_a = dt_d;
+  Datatype target_dtype_b = dt_d;
+  std::int64_t reg_block_a = 0;
+  std::int64_t reg_block_b = 0;
+
+  Scalar alpha{};
+  Scalar beta{};
+  Scalar pack_scale_a{1.0, 0.0, dt_d};
+  Scalar pack_scale_b{1.0, 0.0, dt_d};
+
+  MacroMode macro_mode = MacroMode::Standard;
+  UkrPath ukr_path = UkrPath::Direct;
+  PairAxis pair_axis = PairAxis::None;
+  std::optional<CTempDescriptor> ctemp;
+
+  BlockingParams params{};
+  UkrDescriptor ukr{};
+};
+
+ExecutionPlan plan(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,
+                   const MatrixView& c, const Config& cfg);
+
+// C := alpha*op(A,B) + beta*C on the GPU (dispatch.hpp:89-91).  Synchronous.
+void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,
+          const MatrixView& c, const Config& cfg = Config::defaults(), FlopCounter* fc = nullptr);
+
+// Device-pointer variant ordered on `stream` (a cudaStream_t); returns
+// without synchronising.
+void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,
+                const MatrixView& c, const Config& cfg, void* stream, FlopCounter* fc = nullptr);
+
+// Runs an already-built plan on device operands (the boundary the reference's
+// dispatch.cpp:359-388 crosses).
+void execute(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc = nullptr);
+
+// --------------------------------------------------------------- case labels
+struct CaseLabel {
+  Datatype c = dt_d;
+  Datatype a = dt_d;
+  Datatype b = dt_d;
+  Precision comp = Precision::Double;
+
+  CaseId case_id() const { return classify_case(c.domain, a.domain, b.domain); }
+  std::string str() const;
+  static CaseLabel parse(const std::string& s);
+  static std::vector<CaseLabel> all();
+};
+
+}  // namespace mdgemm

@@ -1,0 +1,160 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes bindings of the CPU checkers.
+
+  * ``orc``  -- oracle/_build/libmdg_oracle.so, the C restatement (mdg_oracle.c)
+  * ``ref``  -- oracle/_ref/libmdgemm_ref.so, the reference engine compiled from
+                its own sources (oracle/Makefile); absent if it was never built.
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs may
+import this module, and only as the checker.  Both libraries take HOST
+pointers and the same plain-data structs as the product ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
+
+from paper_1901_06015_b200 import (ERR, ERR_SCALAR_POLICY, OK, Config, Error, ExecutionPlan, MatrixView, Scalar,
+                                   ScalarPolicyError)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libmdg_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libmdgemm_ref.so")
+
+V, S, C, P = POINTER(MatrixView), Scalar, POINTER(Config), POINTER(ExecutionPlan)
+
+
+def _bind(lib, sig):
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    return lib
+
+
+def _load_orc():
+    if not os.path.exists(ORACLE_SO):
+        raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle oracle`")
+    return _bind(ctypes.CDLL(ORACLE_SO), {
+        "orc_last_error": (c_char_p, []),
+        "orc_rng_split_tag": (c_uint64, [c_uint64, c_char_p]),
+        "orc_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
+        "orc_fill_uniform": (c_int, [V, c_uint64]),
+        "orc_config_defaults": (c_int, [C]),
+        "orc_config_validate": (c_int, [C]),
+        "orc_classify_case": (c_int32, [c_int32, c_int32, c_int32]),
+        "orc_flops_of_case": (c_uint64, [c_int32, c_int64, c_int64, c_int64]),
+        "orc_plan": (c_int, [S, V, V, S, V, C, P]),
+        "orc_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64, c_int64]),
+        "orc_pack": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_int64, c_void_p]),
+        "orc_gemm": (c_int, [S, V, V, S, V, C, POINTER(c_uint64)]),
+        "orc_oracle_gemm": (c_int, [S, V, V, S, V, c_int32, c_void_p]),
+        "orc_violation": (c_int, [S, V, V, S, V, V, c_int32, POINTER(c_double)]),
+    })
+
+
+def _load_ref():
+    if not os.path.exists(REF_SO):
+        return None
+    return _bind(ctypes.CDLL(REF_SO), {
+        "ref_last_error": (c_char_p, []),
+        "ref_config_defaults": (c_int, [C]),
+        "ref_plan": (c_int, [S, V, V, S, V, C, P]),
+        "ref_gemm": (c_int, [S, V, V, S, V, C, POINTER(c_uint64)]),
+        "ref_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64]),
+        "ref_pack": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_void_p, c_size_t]),
+        "ref_oracle_gemm": (c_int, [S, V, V, S, V, c_int32, c_void_p, c_size_t]),
+        "ref_violation": (c_int, [S, V, V, S, V, V, c_int32, POINTER(c_double)]),
+        "ref_fill_uniform_path": (c_int, [V, c_uint64, POINTER(c_char_p), POINTER(c_uint64), c_int32]),
+        "ref_run_bench": (c_int, [c_char_p, c_int64, c_int64, c_int64, c_int32, C, c_uint64,
+                                  POINTER(c_double), POINTER(c_double)]),
+        "ref_flops_of_case": (c_uint64, [c_int32, c_int64, c_int64, c_int64]),
+    })
+
+
+orc = _load_orc()
+ref = _load_ref()
+
+
+def _raise(rc: int, msg: bytes | None):
+    text = (msg or b"").decode(errors="replace")
+    if rc == ERR_SCALAR_POLICY:
+        raise ScalarPolicyError(text)
+    raise Error(text)
+
+
+def check_orc(rc: int) -> None:
+    if rc != OK:
+        _raise(rc, orc.orc_last_error())
+
+
+def check_ref(rc: int) -> None:
+    if rc != OK:
+        _raise(rc, ref.ref_last_error())
+
+
+# ------------------------------------------------------------ convenience
+def orc_plan(alpha, a, b, beta, c, cfg=None) -> ExecutionPlan:
+    out = ExecutionPlan()
+    check_orc(orc.orc_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(out)))
+    return out
+
+
+def ref_plan(alpha, a, b, beta, c, cfg=None) -> ExecutionPlan:
+    out = ExecutionPlan()
+    check_ref(ref.ref_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(out)))
+    return out
+
+
+def orc_gemm(alpha, a, b, beta, c, cfg=None) -> int:
+    flops = c_uint64(0)
+    check_orc(orc.orc_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(flops)))
+    return flops.value
+
+
+def ref_gemm(alpha, a, b, beta, c, cfg=None) -> int:
+    flops = c_uint64(0)
+    check_ref(ref.ref_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(flops)))
+    return flops.value
+
+
+def orc_pack(src, side, fmt, conj, scale, target, reg_block, panel_len, dst_ptr) -> None:
+    check_orc(orc.orc_pack(byref(src), side, fmt, int(conj), scale, target, reg_block, panel_len, c_void_p(dst_ptr)))
+
+
+def ref_pack(src, side, fmt, conj, scale, target, reg_block, dst_ptr, cap) -> None:
+    check_ref(ref.ref_pack(byref(src), side, fmt, int(conj), scale, target, reg_block, c_void_p(dst_ptr), cap))
+
+
+def orc_packed_bytes(src, side, fmt, target, reg_block, panel_len=0) -> int:
+    return orc.orc_packed_bytes(byref(src), side, fmt, target, reg_block, panel_len)
+
+
+def orc_violation(alpha, a, b, beta, c_before, c_after, comp_prec) -> float:
+    v = c_double(0.0)
+    check_orc(orc.orc_violation(alpha, byref(a), byref(b), beta, byref(c_before), byref(c_after), comp_prec, byref(v)))
+    return v.value
+
+
+def ref_violation(alpha, a, b, beta, c_before, c_after, comp_prec) -> float:
+    v = c_double(0.0)
+    check_ref(ref.ref_violation(alpha, byref(a), byref(b), beta, byref(c_before), byref(c_after), comp_prec, byref(v)))
+    return v.value
+
+
+def orc_fill_uniform(v, state: int) -> None:
+    check_orc(orc.orc_fill_uniform(byref(v), c_uint64(state)))
+
+
+def ref_fill_uniform_path(v, seed: int, path) -> None:
+    """Fill through the reference Rng: Rng(seed).split(p0).split(p1)...; str = tag, int = salt."""
+    n = len(path)
+    tags = (c_char_p * max(n, 1))(*[p.encode() if isinstance(p, str) else None for p in path])
+    salts = (c_uint64 * max(n, 1))(*[0 if isinstance(p, str) else int(p) for p in path])
+    check_ref(ref.ref_fill_uniform_path(byref(v), c_uint64(seed), tags, salts, n))
+
+
+def orc_rng_state(seed: int, path) -> int:
+    s = seed & 0xFFFFFFFFFFFFFFFF
+    for p in path:
+        s = orc.orc_rng_split_tag(s, p.encode()) if isinstance(p, str) else orc.orc_rng_split_salt(s, int(p))
+    return s

@@ -1,0 +1,98 @@
+// Plain descriptors passed by value from the host driver to the kernels,
+// plus the host-callable launchers.  No CUDA runtime types in the
+// signatures beyond cudaStream_t.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "mdgemm_b200.h"
+
+namespace mdg {
+
+// A strided typed view in device memory (MatrixView minus planner metadata).
+struct DView {
+  char* base;
+  int64_t m, n, rs, cs;
+  int32_t dtype;
+  int32_t conj;
+};
+
+// Resolved beta of the plan (already rounded to C's storage precision).
+struct DBeta {
+  double re, im;
+  int32_t is_zero, is_one;
+};
+
+// Where accumulated real-image values go: element (r, c) of the me x ne real
+// computation maps onto `out` directly (pair NONE), or pairs rows (2i,2i+1)
+// / columns (2j,2j+1) into one complex element.
+struct DEpilogue {
+  DView out;
+  int32_t pair;
+  int32_t reserved;
+  DBeta beta;
+  int64_t me, ne;
+};
+
+// Panel geometry of one packed operand, in real elements of the computation
+// precision: panels of `pd` rows (left) / columns (right), `lpad` inner-
+// dimension steps each, contiguous pd-vectors per step.
+struct DPanels {
+  const void* data;
+  int64_t pd;
+  int64_t lpad;
+};
+
+struct PackDesc {
+  DView src;
+  int32_t side, format;
+  int32_t do_conj, unit_scale;
+  double sre, sim;
+  int32_t target_single;   // target precision is single
+  int32_t out_complex;     // Standard pack of a complex source: complex elements
+  int64_t pd;              // panel dim in packed-logical units (reg_block)
+  int64_t panels;
+  int64_t len;             // logical panel length
+  int64_t lpad;            // allocated panel length (>= len), zero-filled
+  int64_t ext_i, ext_j;    // source index space incl. panel padding
+};
+
+// Exact (reference-replaying) gemm modes.
+enum ExactMode : int32_t {
+  EXACT_FULL_THEN_COMBINE = 0,  // C_temp: sum from zero over all k, one combine
+  EXACT_DIRECT_SEEDED = 1,      // Direct: accumulators seeded with beta*c in T
+  EXACT_BLOCK_COMBINE = 2,      // Temp without C_temp: combine per KC block
+  EXACT_ONEM_MIXED = 3,         // 1m with complex beta: first KC block through the
+                                // temp tile, later blocks continue in T on the
+                                // flattened C (virtual_ukr_onem re-decides per block)
+};
+
+struct GemmDesc {
+  DPanels a, b;
+  int64_t me, ne, ke;
+  DEpilogue epi;
+  int32_t exact_mode;
+  int32_t reserved;
+  int64_t kc;          // EXACT_BLOCK_COMBINE block length (real inner steps)
+  double seed_beta;    // EXACT_DIRECT_SEEDED: beta as passed to gemm_ukr
+  DView flat;          // EXACT_ONEM_MIXED: real_flatten(C) of the 1m variant
+};
+
+// ---- host launchers (defined in the .cu files) ----
+cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);
+cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s);
+cudaError_t launch_fill_uniform(const DView& v, uint64_t state, cudaStream_t s);
+cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, cudaStream_t s);
+
+// Fast kernels: tile shape chosen by the driver.
+struct FastTile {
+  int bm, bn, bk;
+};
+FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms);
+FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms);
+cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
+cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
+
+}  // namespace mdg

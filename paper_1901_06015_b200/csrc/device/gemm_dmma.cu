@@ -1,0 +1,165 @@
+// FAST numerics, computation precision double: the real microkernel of the
+// reference (ukr_impl<double>, kernels.cpp:7-40) as an sm_100a CTA tile on
+// the FP64 tensor pipe.  tcgen05 has no f64 kind, so the MMA is warp-level
+// DMMA (mma.sync m8n8k4 .f64 -> SASS DMMA.8x8x4).
+//
+// Layout: the pack kernels write Ã / B̃ as panels of BM rows (BN columns)
+// with one contiguous BM-vector (BN-vector) per inner step, so the BK x BM
+// slab a stage needs is ONE contiguous block: a single cp.async.bulk (TMA
+// bulk copy) per operand per stage, completing on an mbarrier.
+//
+// Warp roles: warp NCW (last) is the producer (one elected lane issues the
+// bulk copies into a STAGES-deep ring); warps 0..NCW-1 consume.  After the
+// k loop the accumulator tile is staged through shared memory and every
+// compute thread runs the fused typecast-accumulate epilogue
+// (accumulate_element semantics, kernels.cpp:79-95) straight into C.
+#include "common.cuh"
+
+namespace mdg {
+namespace {
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+struct DmmaCfg {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BK = 16;
+  static constexpr int NCW = WM * WN;
+  static constexpr int THREADS = (NCW + 1) * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int MT = WTM / 8, NT = WTN / 8;
+  static constexpr int STAGE_A = BK * BM, STAGE_B = BK * BN;  // doubles
+  static constexpr size_t RING_BYTES = size_t(STAGES) * (STAGE_A + STAGE_B) * sizeof(double);
+  static constexpr size_t SMEM = RING_BYTES + 2 * STAGES * sizeof(uint64_t);
+  static_assert(size_t(BM) * BN * sizeof(double) <= RING_BYTES, "epilogue tile must fit the ring");
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
+};
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1) gemm_dmma_kernel(GemmDesc d) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = sA + C::STAGES * C::STAGE_A;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);
+  uint64_t* empty = full + C::STAGES;
+
+  const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
+  const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
+  int tm, tn;
+  tile_coords(blockIdx.x, tiles_m, tiles_n, tm, tn);
+  const int64_t lpad = d.a.lpad;
+  const int nk = static_cast<int>(lpad / C::BK);
+  const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
+  const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NCW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == C::NCW) {  // ---------------- producer
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % C::STAGES;
+        if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(double));
+        bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A,
+                 C::STAGE_A * sizeof(double), &full[s]);
+        bulk_g2s(sB + s * C::STAGE_B, Bg + static_cast<int64_t>(kb) * C::STAGE_B,
+                 C::STAGE_B * sizeof(double), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  const int g = lane >> 2, tig = lane & 3;
+  double acc[C::MT][C::NT][2];
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kb = 0; kb < nk; ++kb) {
+    const int s = kb % C::STAGES;
+    mbar_wait(&full[s], (kb / C::STAGES) & 1);
+    const double* a = sA + s * C::STAGE_A + wm * C::WTM + g;
+    const double* b = sB + s * C::STAGE_B + wn * C::WTN + g;
+#pragma unroll
+    for (int kk = 0; kk < C::BK; kk += 4) {
+      double af[C::MT], bf[C::NT];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i) af[i] = a[(kk + tig) * C::BM + i * 8];
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) bf[j] = b[(kk + tig) * C::BN + j * 8];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ------------------------------------------------------------ epilogue
+  constexpr int NCT = C::NCW * 32;
+  named_sync(1, NCT);  // every consumer is done with the ring
+  double* T = reinterpret_cast<double*>(smem);  // BM x BN, column-major
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NT; ++j) {
+      const int r = wm * C::WTM + i * 8 + g;
+      const int c = wn * C::WTN + j * 8 + 2 * tig;
+      T[c * C::BM + r] = acc[i][j][0];
+      T[(c + 1) * C::BM + r] = acc[i][j][1];
+    }
+  named_sync(1, NCT);
+  tile_epilogue(T, C::BM, C::BM, C::BN, static_cast<int64_t>(tm) * C::BM,
+                static_cast<int64_t>(tn) * C::BN, d.epi, threadIdx.x, NCT);
+}
+
+template <class C>
+cudaError_t run(const GemmDesc& d, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(gemm_dmma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(C::SMEM));
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
+  if (tiles == 0) return cudaSuccess;
+  gemm_dmma_kernel<C><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+  return cudaGetLastError();
+}
+
+using Big = DmmaCfg<128, 128, 2, 4, 4>;
+using Small = DmmaCfg<64, 64, 2, 2, 4>;
+
+}  // namespace
+
+FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms) {
+  const int64_t big = ((me + 127) / 128) * ((ne + 127) / 128);
+  if (big >= 4LL * sms) return FastTile{128, 128, 16};
+  const int64_t small = ((me + 63) / 64) * ((ne + 63) / 64);
+  // 3 small CTAs fit per SM; prefer the big tile once it fills the machine
+  // about as evenly as the small one does.
+  const double eff_big = double(big) / (double((big + sms - 1) / sms) * sms);
+  const double eff_small = double(small) / (double((small + 3 * sms - 1) / (3 * sms)) * 3 * sms);
+  return eff_big >= 0.9 * eff_small && big >= sms ? FastTile{128, 128, 16} : FastTile{64, 64, 16};
+}
+
+cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s) {
+  if (t.bm == 128 && t.bn == 128) return run<Big>(d, s);
+  if (t.bm == 64 && t.bn == 64) return run<Small>(d, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace mdg

@@ -1,0 +1,67 @@
+// Small element-wise kernels:
+//  * beta pass for an empty inner dimension (dispatch.cpp:311-317):
+//    C := beta (*) C through the shared combine with t = 0;
+//  * the reference's seeded input generator on the device (rng.hpp:13-56),
+//    so multi-GB benchmark operands are produced in HBM bit-identical to
+//    what Rng/fill_uniform would write on the host.
+#include "common.cuh"
+
+namespace mdg {
+namespace {
+
+__global__ void beta_pass_kernel(DView out, DBeta beta) {
+  const int64_t total = out.m * out.n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    combine_element(out, e % out.m, e / out.m, beta, 0.0, 0.0);
+  }
+}
+
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__device__ __forceinline__ uint64_t splitmix(uint64_t z) {
+  z += kGolden;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Draw number t (0-based) of a stream whose state is s: mix(s + (t+1) * gamma).
+__device__ __forceinline__ double uniform_draw(uint64_t s, uint64_t t) {
+  const uint64_t x = splitmix(s + (t + 1) * kGolden);
+  return 2.0 * (static_cast<double>(x >> 11) * 0x1p-53) - 1.0;
+}
+
+__global__ void fill_uniform_kernel(DView v, uint64_t state) {
+  const int64_t total = v.m * v.n;
+  const bool cplx = dt_complex(v.dtype);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % v.m, j = e / v.m;  // column-major draw order
+    const uint64_t t = static_cast<uint64_t>(j * v.m + i) * (cplx ? 2u : 1u);
+    const double re = uniform_draw(state, t);
+    const double im = cplx ? uniform_draw(state, t + 1) : 0.0;
+    st_elem(v, i, j, re, im);
+  }
+}
+
+int grid_for(int64_t total) {
+  const int64_t blocks = (total + 255) / 256;
+  return static_cast<int>(blocks < 148 * 32 ? (blocks > 0 ? blocks : 1) : 148 * 32);
+}
+
+}  // namespace
+
+cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s) {
+  if (out.m * out.n == 0) return cudaSuccess;
+  beta_pass_kernel<<<grid_for(out.m * out.n), 256, 0, s>>>(out, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_uniform(const DView& v, uint64_t state, cudaStream_t s) {
+  if (v.m * v.n == 0) return cudaSuccess;
+  fill_uniform_kernel<<<grid_for(v.m * v.n), 256, 0, s>>>(v, state);
+  return cudaGetLastError();
+}
+
+}  // namespace mdg

@@ -1,0 +1,331 @@
+// Execution half of gemm() on the GPU: replaces the reference's
+// gemm_blocked + C_temp + write_back + beta_pass (dispatch.cpp:359-388,
+// gemm_core.cpp:74-185).  Host C++ only: it sizes the packed panels, launches
+// the pack kernels and one gemm kernel per call, and keeps the reference's
+// FlopCounter accounting.
+#include "driver.hpp"
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+namespace mdgemm {
+
+namespace {
+
+int device_sms() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() <= static_cast<size_t>(dev)) cache.resize(dev + 1, 0);
+  if (cache[dev] == 0) {
+    int sms = 0;
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+    // Keep stream-ordered workspace cached between calls.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cache[dev] = sms;
+  }
+  return cache[dev];
+}
+
+int32_t dt_code(Datatype t) {
+  return (t.domain == Domain::Complex ? 2 : 0) + (t.precision == Precision::Double ? 1 : 0);
+}
+
+mdg::DBeta to_dbeta(const Scalar& b) {
+  return mdg::DBeta{b.re, b.im, b.is_zero() ? 1 : 0, b.is_one() ? 1 : 0};
+}
+
+// Packed operand consumed by a kernel tile of `tile` real rows (left) or
+// columns (right); a complex operand packed Standard counts complex rows.
+struct Packed {
+  mdg::PackDesc desc{};
+  size_t bytes = 0;
+};
+
+Packed prepare_pack(const MatrixView& src, Side side, PackFormat fmt, bool conj, const Scalar& scale,
+                    Datatype target, int64_t tile, int64_t lpad) {
+  const bool halves = fmt == PackFormat::Standard && src.dtype.domain == Domain::Complex;
+  Packed out;
+  out.desc = make_pack_desc(src, side, fmt, conj, scale, target, halves ? tile / 2 : tile, lpad, &out.bytes);
+  return out;
+}
+
+bool onem_direct(const ExecutionPlan& p) {
+  const FlattenAxis ax = p.ukr_path == UkrPath::OneMColumn ? FlattenAxis::Rows : FlattenAxis::Cols;
+  return p.beta.im == 0.0 && p.c.dtype.precision == p.comp_prec && can_flatten(p.c, ax);
+}
+
+}  // namespace
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+mdg::DView to_dview(const MatrixView& v) {
+  return mdg::DView{reinterpret_cast<char*>(v.base), v.m, v.n, v.rs, v.cs, dt_code(v.dtype), v.conj ? 1 : 0};
+}
+
+PackGeometry pack_geometry(const MatrixView& src, Side side, PackFormat format, Datatype target,
+                           int64_t reg_block, int64_t panel_len) {
+  if (reg_block < 1) throw Error("pack_block: reg_block must be at least 1");
+  const bool left = side == Side::Left;
+  PackGeometry g;
+  int64_t rows = 0, cols = 0;
+  switch (format) {
+    case PackFormat::Standard:
+      if (target.domain != src.dtype.domain) throw Error("pack_block: Standard packing cannot change the domain");
+      g.block_dtype = target;
+      rows = src.m;
+      cols = src.n;
+      break;
+    case PackFormat::OneE:
+      if (src.dtype.domain != Domain::Complex) throw Error("pack_block: OneE requires a complex source");
+      if (reg_block % 2) throw Error("pack_block: OneE requires an even reg_block");
+      g.block_dtype = Datatype{Domain::Real, target.precision};
+      rows = 2 * src.m;
+      cols = 2 * src.n;
+      break;
+    case PackFormat::OneR:
+      if (src.dtype.domain != Domain::Complex) throw Error("pack_block: OneR requires a complex source");
+      g.block_dtype = Datatype{Domain::Real, target.precision};
+      rows = left ? src.m : 2 * src.m;
+      cols = left ? 2 * src.n : src.n;
+      break;
+  }
+  const int64_t extent = left ? rows : cols;
+  g.panels = (extent + reg_block - 1) / reg_block;
+  g.len = left ? cols : rows;
+  g.lpad = std::max(g.len, panel_len);
+  g.bytes = static_cast<size_t>(g.panels * reg_block * g.lpad) * dtype_size(g.block_dtype);
+  return g;
+}
+
+uint64_t reference_flops(const ExecutionPlan& p) {
+  if (p.m <= 0 || p.n <= 0 || p.k <= 0) return 0;
+  const uint64_t MR = static_cast<uint64_t>(p.ukr.mr), NR = static_cast<uint64_t>(p.ukr.nr);
+  const uint64_t tiles = static_cast<uint64_t>((p.m + p.ukr.mr - 1) / p.ukr.mr) *
+                         static_cast<uint64_t>((p.n + p.ukr.nr - 1) / p.ukr.nr);
+  uint64_t total = 2 * MR * NR * static_cast<uint64_t>(p.k) * tiles;
+  // gemm_ukr adds mr*nr when called directly with beta not in {0,1}
+  // (kernels.cpp:73-76): the Direct path and 1m-direct, first KC block only.
+  bool direct_ukr = false;
+  if (!p.ctemp) {
+    if (p.ukr_path == UkrPath::Direct) direct_ukr = true;
+    if ((p.ukr_path == UkrPath::OneMColumn || p.ukr_path == UkrPath::OneMRow) && onem_direct(p))
+      direct_ukr = true;
+  }
+  if (direct_ukr && p.beta.re != 0.0 && p.beta.re != 1.0) total += MR * NR * tiles;
+  return total;
+}
+
+void pack_block_device(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
+                       Scalar scale, Datatype target, std::int64_t reg_block, void* stream) {
+  pack_block_device_padded(dst, src, side, format, conj, scale, target, reg_block, 0, stream);
+}
+
+mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format, bool conj,
+                             const Scalar& scale, Datatype target, int64_t reg_block, int64_t panel_len,
+                             size_t* bytes) {
+  if (scale.im != 0.0 && format == PackFormat::Standard)
+    throw Error("pack_block: complex scale requires OneE or OneR format");
+  const PackGeometry g = pack_geometry(src, side, format, target, reg_block, panel_len);
+  mdg::PackDesc d{};
+  d.src = to_dview(src);
+  d.side = side == Side::Left ? MDG_SIDE_LEFT : MDG_SIDE_RIGHT;
+  d.format = static_cast<int32_t>(format);
+  d.do_conj = src.conj != conj;  // packing.cpp:140
+  d.unit_scale = scale.is_one();
+  d.sre = scale.re;
+  d.sim = scale.im;
+  d.target_single = target.precision == Precision::Single;
+  d.out_complex = g.block_dtype.domain == Domain::Complex;
+  d.pd = reg_block;
+  d.panels = g.panels;
+  d.len = g.len;
+  d.lpad = g.lpad;
+  // Source index space covered by the kernel, panel padding included.
+  const int64_t src_units = format == PackFormat::OneE ? reg_block / 2 : reg_block;
+  d.ext_i = side == Side::Left ? g.panels * src_units : src.m;
+  d.ext_j = side == Side::Left ? src.n : g.panels * src_units;
+  if (bytes) *bytes = g.bytes;
+  return d;
+}
+
+void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
+                              Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
+                              void* stream) {
+  const mdg::PackDesc d = make_pack_desc(src, side, format, conj, scale, target, reg_block, panel_len, nullptr);
+  cuda_check(mdg::launch_pack(d, dst, static_cast<cudaStream_t>(stream)), "pack kernel");
+}
+
+std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Datatype target,
+                         std::int64_t reg_block) {
+  return pack_geometry(src, side, format, target, reg_block, 0).bytes;
+}
+
+void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
+  if (p.m == 0 || p.n == 0) return;
+  if (p.k == 0) {
+    if (!p.beta.is_one())
+      cuda_check(mdg::launch_beta_pass(to_dview(p.c), to_dbeta(p.beta), st), "beta pass");
+    return;
+  }
+  const bool single = p.comp_prec == Precision::Single;
+  const bool exact = numerics == Numerics::Exact;
+  const int sms = device_sms();
+
+  mdg::FastTile tile{64, 64, 1};
+  if (!exact) tile = single ? mdg::choose_ffma_tile(p.m, p.n, sms) : mdg::choose_dmma_tile(p.m, p.n, sms);
+  const int64_t lpad = (p.k + tile.bk - 1) / tile.bk * tile.bk;
+
+  Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, tile.bm, lpad);
+  Packed pb = prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, tile.bn, lpad);
+
+  const size_t off_b = (pa.bytes + 255) / 256 * 256;
+  void* ws = nullptr;
+  cuda_check(cudaMallocAsync(&ws, off_b + pb.bytes, st), "workspace allocation");
+  char* wsa = static_cast<char*>(ws);
+  cudaError_t err = mdg::launch_pack(pa.desc, wsa, st);
+  if (err == cudaSuccess) err = mdg::launch_pack(pb.desc, wsa + off_b, st);
+
+  mdg::GemmDesc g{};
+  g.a = mdg::DPanels{wsa, tile.bm, lpad};
+  g.b = mdg::DPanels{wsa + off_b, tile.bn, lpad};
+  g.me = p.m;
+  g.ne = p.n;
+  g.ke = p.k;
+  g.epi.out = to_dview(p.c);
+  g.epi.pair = static_cast<int32_t>(p.pair_axis);
+  g.epi.beta = to_dbeta(p.beta);
+  g.epi.me = p.m;
+  g.epi.ne = p.n;
+  g.kc = p.params.kc;
+  g.seed_beta = p.beta.re;
+
+  if (err == cudaSuccess) {
+    if (exact) {
+      // Replay the reference's output path for this plan.
+      g.exact_mode = mdg::EXACT_BLOCK_COMBINE;
+      const bool onem = p.ukr_path == UkrPath::OneMColumn || p.ukr_path == UkrPath::OneMRow;
+      const FlattenAxis ax = p.ukr_path == UkrPath::OneMColumn ? FlattenAxis::Rows : FlattenAxis::Cols;
+      const bool onem_flat = onem && p.c.dtype.precision == p.comp_prec && can_flatten(p.c, ax);
+      if (p.ctemp) {
+        g.exact_mode = mdg::EXACT_FULL_THEN_COMBINE;
+      } else if (p.ukr_path == UkrPath::Direct) {
+        g.exact_mode = mdg::EXACT_DIRECT_SEEDED;
+      } else if (onem_flat && p.beta.im == 0.0) {
+        g.exact_mode = mdg::EXACT_DIRECT_SEEDED;
+        g.epi.out = to_dview(real_flatten(p.c, ax));
+        g.epi.pair = MDG_PAIR_NONE;
+      } else if (onem_flat) {
+        g.exact_mode = mdg::EXACT_ONEM_MIXED;
+        g.flat = to_dview(real_flatten(p.c, ax));
+      }
+      err = mdg::launch_gemm_exact(g, single, st);
+    } else {
+      err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+    }
+  }
+  const cudaError_t ferr = cudaFreeAsync(ws, st);
+  cuda_check(err, "gemm kernels");
+  cuda_check(ferr, "workspace release");
+  if (fc) fc->add(reference_flops(p));
+}
+
+// ----------------------------------------------------------------- gemm()
+
+namespace {
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+struct Staged {
+  const std::byte* lo = nullptr;
+  const std::byte* hi = nullptr;
+  std::byte* dev = nullptr;
+};
+
+}  // namespace
+
+void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
+                const Config& cfg, void* stream, FlopCounter* fc) {
+  if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
+  const ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
+  execute(p, cfg.numerics, stream, fc);
+}
+
+void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
+          const Config& cfg, FlopCounter* fc) {
+  if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
+  ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
+  cudaStream_t st = cudaStreamPerThread;
+  if (p.m == 0 || p.n == 0) return;
+
+  // Host operands are staged through HBM: copy each operand's byte window,
+  // rebase the plan's views into the copies, copy C's window back.
+  const MatrixView* originals[3] = {&a, &b, &c};
+  const bool need[3] = {p.k > 0, p.k > 0, true};
+  Staged stg[3];
+  bool any_host = false;
+  for (int i = 0; i < 3; ++i) {
+    const auto [lo, hi] = byte_range(*originals[i]);
+    stg[i].lo = lo;
+    stg[i].hi = hi;
+    if (need[i] && hi > lo && !is_device_ptr(lo)) any_host = true;
+  }
+  std::vector<void*> allocations;
+  auto release = [&] {
+    for (void* q : allocations) cudaFreeAsync(q, st);
+    cudaStreamSynchronize(st);
+  };
+  try {
+    if (any_host) {
+      for (int i = 0; i < 3; ++i) {
+        if (!need[i] || stg[i].hi <= stg[i].lo || is_device_ptr(stg[i].lo)) continue;
+        const size_t bytes = static_cast<size_t>(stg[i].hi - stg[i].lo);
+        void* d = nullptr;
+        cuda_check(cudaMallocAsync(&d, bytes, st), "staging allocation");
+        allocations.push_back(d);
+        stg[i].dev = static_cast<std::byte*>(d);
+        cuda_check(cudaMemcpyAsync(d, stg[i].lo, bytes, cudaMemcpyHostToDevice, st), "H2D staging");
+      }
+      auto rebase = [&](MatrixView& v) {
+        for (int i = 0; i < 3; ++i)
+          if (stg[i].dev && v.base >= stg[i].lo && v.base < stg[i].hi) {
+            v.base = stg[i].dev + (v.base - stg[i].lo);
+            return;
+          }
+      };
+      rebase(p.a);
+      rebase(p.b);
+      rebase(p.c);
+    }
+    execute(p, cfg.numerics, st, fc);
+    if (stg[2].dev)
+      cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(stg[2].lo), stg[2].dev,
+                                 static_cast<size_t>(stg[2].hi - stg[2].lo), cudaMemcpyDeviceToHost, st),
+                 "D2H staging");
+    cuda_check(cudaStreamSynchronize(st), "gemm synchronisation");
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+}
+
+}  // namespace mdgemm

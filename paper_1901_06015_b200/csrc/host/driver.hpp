@@ -1,0 +1,45 @@
+// Internal host-side declarations shared by the driver and the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../device/desc.h"
+#include "mdgemm/mdgemm.hpp"
+
+namespace mdgemm {
+
+// CUDA runtime failure, surfaced across the C ABI as MDG_ERR_CUDA.
+struct CudaFailure : Error {
+  explicit CudaFailure(const std::string& what) : Error(what) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+mdg::DView to_dview(const MatrixView& v);
+
+// resolve_geometry (packing.cpp:27-67) plus an optional padded panel length.
+struct PackGeometry {
+  Datatype block_dtype = dt_d;
+  int64_t panels = 0;
+  int64_t len = 0;   // logical panel length
+  int64_t lpad = 0;  // allocated panel length
+  size_t bytes = 0;
+};
+PackGeometry pack_geometry(const MatrixView& src, Side side, PackFormat format, Datatype target,
+                           int64_t reg_block, int64_t panel_len);
+
+mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format, bool conj,
+                             const Scalar& scale, Datatype target, int64_t reg_block, int64_t panel_len,
+                             size_t* bytes);
+
+void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
+                              Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
+                              void* stream);
+
+// The value the reference's FlopCounter reaches for this plan.
+uint64_t reference_flops(const ExecutionPlan& p);
+
+}  // namespace mdgemm

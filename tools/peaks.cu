@@ -1,0 +1,166 @@
+// Peak-throughput microbenchmarks for the arithmetic pipes the mixed-datatype
+// gemm uses on sm_100a: FP64 DFMA (SIMT), FP64 DMMA (mma.sync .f64, several
+// shapes), FP32 FFMA (SIMT).  Every kernel runs independent dependency chains
+// so the pipe, not latency, is the limit.  Prints one JSON object.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); return 1; } } while (0)
+
+constexpr int ITERS = 4096;
+
+__global__ void k_dfma(double* out, double s) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], s, 0.5);
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += a[i];
+  if (r == 1234.5) out[0] = r;
+}
+
+__global__ void k_ffma(float* out, float s) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], s, 0.5f);
+  }
+  float r = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r += a[i];
+  if (r == 1234.5f) out[0] = r;
+}
+
+// m8n8k4: A 1 f64, B 1 f64, C 2 f64 per thread.
+__global__ void k_dmma_884(double* out) {
+  double a = threadIdx.x * 1e-3, b = 0.5;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0;
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+  if (r == 1234.5) out[0] = r;
+}
+
+// m16n8k4: A 2, B 1, C 4.
+__global__ void k_dmma_1684(double* out) {
+  double a0 = threadIdx.x * 1e-3, a1 = 0.25, b = 0.5;
+  double c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
+  for (int it = 0; it < ITERS / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0), "d"(a1), "d"(b));
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (r == 1234.5) out[0] = r;
+}
+
+// m16n8k8: A 4, B 2, C 4.
+__global__ void k_dmma_1688(double* out) {
+  double a0 = threadIdx.x * 1e-3, a1 = 0.25, a2 = 0.125, a3 = 0.3, b0 = 0.5, b1 = 0.7;
+  double c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
+  for (int it = 0; it < ITERS / 8; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                   : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (r == 1234.5) out[0] = r;
+}
+
+// m16n8k16: A 8, B 4, C 4.
+__global__ void k_dmma_16816(double* out) {
+  double a[8], b[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = 0.5 + i;
+  double c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
+  for (int it = 0; it < ITERS / 16; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+  }
+  double r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1] + c[i][2] + c[i][3];
+  if (r == 1234.5) out[0] = r;
+}
+
+template <typename F>
+static float time_it(F launch, int reps) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  launch(); launch();
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  return best;
+}
+
+int main(int argc, char** argv) {
+  int sms = 0, clk = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0));
+  double* dout; float* fout;
+  CK(cudaMalloc(&dout, 64)); CK(cudaMalloc(&fout, 64));
+  int reps = argc > 1 ? atoi(argv[1]) : 20;
+  printf("{\"sms\": %d, \"clock_khz_attr\": %d", sms, clk);
+  for (int wpb : {4, 8, 16}) {
+    dim3 grid(sms * 4), block(32 * wpb);
+    double nthr = double(grid.x) * block.x;
+    float ms = time_it([&] { k_dfma<<<grid, block>>>(dout, 0.999); }, reps);
+    printf(", \"dfma_w%d_tflops\": %.3f", wpb, nthr * ITERS * 8 * 2 / (ms * 1e-3) / 1e12);
+    ms = time_it([&] { k_ffma<<<grid, block>>>(fout, 0.999f); }, reps);
+    printf(", \"ffma_w%d_tflops\": %.3f", wpb, nthr * ITERS * 16 * 2 / (ms * 1e-3) / 1e12);
+    double nwarps = double(grid.x) * wpb;
+    ms = time_it([&] { k_dmma_884<<<grid, block>>>(dout); }, reps);
+    printf(", \"dmma884_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 4) * 8 * (8 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
+    ms = time_it([&] { k_dmma_1684<<<grid, block>>>(dout); }, reps);
+    printf(", \"dmma1684_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 4) * 4 * (16 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
+    ms = time_it([&] { k_dmma_1688<<<grid, block>>>(dout); }, reps);
+    printf(", \"dmma1688_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 8) * 4 * (16 * 8 * 8 * 2) / (ms * 1e-3) / 1e12);
+    ms = time_it([&] { k_dmma_16816<<<grid, block>>>(dout); }, reps);
+    printf(", \"dmma16816_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 16) * 4 * (16 * 8 * 16 * 2) / (ms * 1e-3) / 1e12);
+  }
+  CK(cudaGetLastError());
+  printf("}\n");
+  return 0;
+}
