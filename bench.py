@@ -1,0 +1,435 @@
+#!/usr/bin/env python3
+"""bench.py -- throughput of the B200 mixed-datatype gemm (arXiv 1901.06015).
+
+Metric (BASELINE.json): effective GFLOPS = sum of flops_of_case(label, m, n, k)
+(2/4/8 mnk, dispatch.cpp:35-54) / time, and its fraction of the measured
+FP64-DMMA / FP32-FFMA peak.
+
+Default workload = BASELINE configs[1], the 128-label sweep, at its largest
+size m=n=k=4096: one step runs all 128 cabx labels once with the sweep's
+scalars (alpha = 1.2-0.7i for cases 0 and 3, real 1.2 for the six cases that
+reject a complex alpha; beta = 0.9+0.3i), A/B/C column-major, entries
+uniform[-1,1) from the reference's splitmix64 Rng (generated on the device).
+Other BASELINE configs are available with --workload.
+
+Multi-GPU (torchrun): C and B are split into column panels per rank
+(mdg_shard_columns), A is broadcast from rank 0 over NCCL inside every step;
+no reduction.  Strong scaling (fixed total problem).
+
+Arms:
+  --impl b200       (default) this framework, device-resident operands
+                    (value) and through the public gemm() with pinned host
+                    buffers, H2D + D2H inside the timed region (e2e).
+  --impl reference  the reference CPU engine (oracle/_ref, compiled from the
+                    reference's own sources) on the host cores, rank 0 only,
+                    on a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "effective GFLOPS and % of FP64/FP32 peak per mixed-datatype gemm case, 1/2/4/8 GPU"
+PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks_r01.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default="sweep",
+                    choices=["sweep", "cfg1", "cfg3", "cfg4-cdds", "cfg4-szzs", "cfg4-zczd",
+                             "cfg5-k64", "cfg5-k256", "cfg5-k1024"])
+    ap.add_argument("--size", type=int, default=4096, help="sweep size m=n=k")
+    ap.add_argument("--labels", default="", help="comma-separated subset of labels (sweep)")
+    ap.add_argument("--numerics", choices=["fast", "exact"], default="fast")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-size", type=int, default=512, help="sample size of the CPU baseline")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workloads
+def workload(args):
+    """(description, [(label, m, n, k, alpha, beta)], distribution)."""
+    import paper_1901_06015_b200 as M
+    S = M.Scalar
+    if args.workload == "sweep":
+        labels = [l.str() for l in M.CaseLabel.all()]
+        if args.labels:
+            labels = [l for l in args.labels.split(",") if l]
+        items = []
+        for lab in labels:
+            cid = M.CaseLabel.parse(lab).case_id()
+            alpha = S.complex_value(1.2, -0.7) if cid in (0, 7) else S.real_value(1.2)
+            items.append((lab, args.size, args.size, args.size, alpha, S.complex_value(0.9, 0.3)))
+        desc = (f"BASELINE configs[1]: {len(labels)}-label sweep at m=n=k={args.size}, column-major, "
+                "alpha=1.2-0.7i (cases 0,3; real 1.2 otherwise), beta=0.9+0.3i")
+        return desc, items, "uniform"
+    if args.workload == "cfg1":
+        return ("BASELINE configs[0]: dssd m=n=k=1024, alpha=beta=1",
+                [("dssd", 1024, 1024, 1024, S.real_value(1.0), S.real_value(1.0))], "uniform")
+    if args.workload == "cfg3":
+        return ("BASELINE configs[2]: zzzd 1m, m=n=k=8192, alpha=0.5+1.5i, beta=1",
+                [("zzzd", 8192, 8192, 8192, S.complex_value(0.5, 1.5), S.real_value(1.0))], "uniform")
+    if args.workload.startswith("cfg4"):
+        lab = args.workload.split("-")[1]
+        return (f"BASELINE configs[3]: {lab} m=n=k=16384, beta=0",
+                [(lab, 16384, 16384, 16384, S.real_value(1.0), S.real_value(0.0))], "uniform")
+    k = int(args.workload.split("-k")[1])
+    return (f"BASELINE configs[4]: sddd rank-k update m=n=32768 k={k}, alpha=-1, beta=1",
+            [("sddd", 32768, 32768, k, S.real_value(-1.0), S.real_value(1.0))], "normal")
+
+
+def useful_flops(items):
+    import paper_1901_06015_b200 as M
+    return sum(M.flops_of_case(M.CaseLabel.parse(l).case_id(), m, n, k) for l, m, n, k, _, _ in items)
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(device_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.file, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        rows = []
+        for line in open(self.file.name):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.file.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------- peak numbers
+def peaks():
+    with open(PEAKS_FILE) as f:
+        p = json.load(f)
+    hbm = None
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        hbm = json.load(open(mp)).get("hbm_gbs")
+    return {"dmma_tflops": p["dmma_tflops"], "ffma_tflops": p["ffma_tflops"], "hbm_gbs": hbm or 6650.0,
+            "hbm_source": "MEASURED_PEAKS.json" if hbm else "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------ b200 arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_06015_b200 as M
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    desc, items, dist_kind = workload(args)
+    cfg = M.Config.defaults().set("gpu.numerics", args.numerics)
+
+    # ---- operands: one A/B/C per distinct (role, dtype, shape); B, C column panels per rank
+    def alloc(dtype, m, n):
+        t = torch.empty(max(m * n, 1) * M.dtype_size(dtype), dtype=torch.uint8, device=dev)
+        return t, M.MatrixView.make(t.data_ptr(), m, n, 1, max(m, 1), dtype)
+
+    ops = {}
+    a_bufs = []
+    shard = {}
+    for lab, m, n, k, _, _ in items:
+        j0, nb = M.shard_columns(n, world, rank, 128)
+        shard[(lab, m, n, k)] = (j0, nb)
+        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
+        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, nb)), ("c", dc, (m, nb))):
+            key = (role, dt, shape)
+            if key not in ops:
+                t, v = alloc(dt, *shape)
+                tag = f"{args.workload}/{role}/{M.dtype_letter(dt)}/{shape}/r{0 if role == 'a' else rank}"
+                if dist_kind == "normal":  # normal(0,1) per real component, seeded per operand
+                    g = torch.Generator(device=dev).manual_seed(len(ops) * 7919 + 13 * (rank if role != "a" else 0))
+                    real = torch.float32 if M.precision_of(dt) == M.SINGLE else torch.float64
+                    flat = t.view(real)
+                    flat.copy_(torch.randn(flat.numel(), generator=g, device=dev, dtype=real))
+                else:
+                    M.fill_uniform(v, M.Rng(args.seed).split(tag).state, stream)
+                ops[key] = (t, v)
+                if role == "a":
+                    a_bufs.append(t)
+    calls = []
+    for lab, m, n, k, al, be in items:
+        j0, nb = shard[(lab, m, n, k)]
+        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
+        comp = M.SINGLE if lab[3] == "s" else M.DOUBLE
+        va = ops[("a", da, (m, k))][1]
+        vb = ops[("b", db, (k, nb))][1]
+        vc = ops[("c", dc, (m, nb))][1].with_comp_prec(comp)
+        if nb > 0:
+            calls.append((al, va, vb, be, vc))
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def step():
+        if world > 1:
+            for t in a_bufs:
+                dist.broadcast(t, src=0)
+        for al, va, vb, be, vc in calls:
+            M.gemm_async(al, va, vb, be, vc, cfg, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    launches0 = M.launch_count()
+    M.profile_begin()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between timed steps (outside the events)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    kstats = M.profile_end()
+    launches = M.launch_count() - launches0
+    clocks = sampler.stop()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+
+    flops = useful_flops(items) * args.steps
+    value = flops / (total_ms * 1e-3) / 1e9
+    pk = peaks()
+    # time the whole job would take at the measured per-GPU peaks
+    ideal_s = sum(M.flops_of_case(M.CaseLabel.parse(l).case_id(), m, n, k) /
+                  ((pk["ffma_tflops"] if l[3] == "s" else pk["dmma_tflops"]) * 1e12 * world)
+                  for l, m, n, k, _, _ in items) * args.steps
+    peak_fraction = ideal_s / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel (rank 0's launches)
+    dom = max(("dmma", "ffma", "pack"), key=lambda k: kstats[k]["ms"])
+    ks = kstats[dom]
+    traffic = None
+    if os.path.exists(TRAFFIC_FILE):
+        traffic = json.load(open(TRAFFIC_FILE)).get(dom)
+    if dom == "pack":
+        achieved = ks["work"] / (ks["ms"] * 1e-3) / 1e9 if ks["ms"] else 0.0
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "pack",
+                "peak_source": pk["hbm_source"]}
+    else:
+        achieved = ks["work"] / (ks["ms"] * 1e-3) / 1e12 if ks["ms"] else 0.0
+        peak = pk["dmma_tflops"] if dom == "dmma" else pk["ffma_tflops"]
+        roof = {"bound": "tensor" if dom == "dmma" else "fp32-simt", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "kernel": "gemm_dmma (DMMA.8x8x4 fp64 tensor pipe)" if dom == "dmma" else "gemm_ffma (FFMA fp32)",
+                "peak_source": "measured: tools/peaks.cu on this pool's B200 (profiles/peaks_r01.json)",
+                "algorithmic_work": "2*me*ne*ke real flops per launch (= flops_of_case, the 1m reduction has no waste)"}
+    kernel_share = {k: round(v["ms"] / total_ms, 4) if total_ms else 0 for k, v in kstats.items() if v["launches"]}
+
+    # ---- e2e: public gemm() on pinned host buffers, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for key, (t, v) in ops.items():
+            h = torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True)
+            h.copy_(t)
+            hv = M.MatrixView.from_buffer_copy(v)
+            hv.base = h.data_ptr()
+            host[key] = (h, hv)
+        hcalls, h2d, d2h = [], 0, 0
+        for lab, m, n, k, al, be in items:
+            j0, nb = shard[(lab, m, n, k)]
+            if nb == 0:
+                continue
+            dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
+            comp = M.SINGLE if lab[3] == "s" else M.DOUBLE
+            ha, hb, hc = host[("a", da, (m, k))], host[("b", db, (k, nb))], host[("c", dc, (m, nb))]
+            hcalls.append((al, ha[1], hb[1], be, hc[1].with_comp_prec(comp)))
+            h2d += ha[0].numel() + hb[0].numel() + hc[0].numel()
+            d2h += hc[0].numel()
+        torch.cuda.synchronize()
+        M.gemm(*hcalls[0][:5], cfg)  # warm the staging pool
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for al, va, vb, be, vc in hcalls:
+                M.gemm(al, va, vb, be, vc, cfg)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": flops / el / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": d2h * world, "api": "mdgemm gemm() / mdg_gemm with pinned host MatrixViews",
+               "timer": "host wall clock around synchronous calls"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (per label computation precision)",
+        "data": "synthetic: reference splitmix64 Rng uniform[-1,1) generated on device"
+                if dist_kind == "uniform" else "synthetic: normal(0,1) from a seeded device generator",
+        "config": {"workload": desc, "labels": len(items), "numerics": args.numerics,
+                   "parallelism": f"column panels x{world}, A broadcast over NCCL" if world > 1 else "single GPU",
+                   "l2": "operands > L2 per step and a 512 MiB L2 flush between timed steps"},
+        "peak_fraction": peak_fraction,
+        "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},
+        "roofline": roof,
+        "kernel_share": kernel_share,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+    }
+    if not args.no_cpu and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------- reference arm
+def reference_sample(args):
+    import paper_1901_06015_b200 as M
+    desc, items, _ = workload(args)
+    if args.workload == "sweep":
+        s = args.cpu_size
+        sample = [(l, s, s, s, al, be) for l, _, _, _, al, be in items]
+        text = f"all {len(sample)} sweep labels at m=n=k={s}"
+    else:
+        sample, text = [], ""
+        for l, m, n, k, al, be in items:  # a column/row sub-block with the full inner dimension
+            mm, nn = min(m, 512), min(n, 512)
+            sample.append((l, mm, nn, k, al, be))
+            text = f"{l} sub-block {mm}x{nn} with the full k={k}"
+    return desc, sample, text
+
+
+def run_reference_steps(args, steps, warmup):
+    """Times the reference engine (oracle/_ref, built from the reference sources) through its
+    public gemm() on host memory, all host threads, ctemp=on."""
+    import paper_1901_06015_b200 as M
+    from oracle import oracle as O
+    from tests.helpers import HostMatrix
+
+    if O.ref is None:
+        raise RuntimeError("oracle/_ref/libmdgemm_ref.so is missing")
+    cores = os.cpu_count() or 1
+    cfg = M.Config.defaults().set("gemm.threads", cores).set("ctemp.enable", "on")
+    desc, sample, text = reference_sample(args)
+    mats = {}
+    calls = []
+    for l, m, n, k, al, be in sample:
+        dc, da, db = (M.dtype_from_letter(ch) for ch in l[:3])
+        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, n)), ("c", dc, (m, n))):
+            if (role, dt, shape) not in mats:
+                mats[(role, dt, shape)] = HostMatrix(dt, *shape).fill(O.orc_rng_state(args.seed, [role, dt, *shape]))
+        comp = M.SINGLE if l[3] == "s" else M.DOUBLE
+        calls.append((al, mats[("a", da, (m, k))].view(), mats[("b", db, (k, n))].view(), be,
+                      mats[("c", dc, (m, n))].view(comp=comp)))
+    flops = useful_flops(sample)
+    for _ in range(warmup):
+        for c in calls:
+            O.ref_gemm(*c, cfg)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        for c in calls:
+            O.ref_gemm(*c, cfg)
+        times.append(time.perf_counter() - t0)
+    return desc, text, flops, times, cores
+
+
+def cpu_baseline(args):
+    try:
+        _, text, flops, times, cores = run_reference_steps(args, 1, 1)
+    except Exception as e:  # noqa: BLE001 - reported, not fatal for the GPU line
+        return {"value": None, "unit": "GFLOPS", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+    return {"value": flops / times[0] / 1e9, "unit": "GFLOPS", "cores": cores, "kind": "reference",
+            "sample": f"{text}; reference gemm() (oracle/_ref) with gemm.threads={cores}, ctemp.enable=on; "
+                      f"1 warm-up + 1 timed pass ({times[0]:.1f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    desc, text, flops, times, cores = run_reference_steps(args, args.steps, args.warmup)
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOPS",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64/f32 (per label computation precision)", "data": "synthetic: reference Rng uniform[-1,1)",
+        "config": {"workload": desc, "numerics": "reference CPU engine"},
+        "cpu_baseline": {"value": value, "unit": "GFLOPS", "cores": cores, "kind": "reference",
+                         "sample": f"{text}; reference gemm() with gemm.threads={cores}, ctemp.enable=on"},
+        "e2e": {"value": value, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -201,6 +201,28 @@ uint64_t mdg_rng_split_salt(uint64_t state, uint64_t salt);
 int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align,
                       int64_t* j0, int64_t* nb);
 
+/* ---- instrumentation (the reference's FlopCounter, extended per kernel) ---
+ * Every kernel the library launches bumps a process-wide counter.  Between
+ * mdg_profile_begin() and mdg_profile_end() the calling thread also brackets
+ * each launch with CUDA events on its stream (no synchronisation until
+ * _end), and _end reports per kernel kind: launches, summed device time and
+ * the algorithmic work (flops for gemm kernels, bytes read + written for
+ * pack / beta kernels). */
+enum {
+  MDG_KERNEL_PACK = 0, MDG_KERNEL_DMMA = 1, MDG_KERNEL_FFMA = 2, MDG_KERNEL_EXACT = 3,
+  MDG_KERNEL_BETA = 4, MDG_KERNEL_FILL = 5, MDG_KERNEL_KINDS = 6
+};
+
+typedef struct mdg_kernel_stats {
+  uint64_t launches;
+  double total_ms;
+  double work;
+} mdg_kernel_stats_t;
+
+uint64_t mdg_launch_count(void);
+int mdg_profile_begin(void);
+int mdg_profile_end(mdg_kernel_stats_t* out /* [MDG_KERNEL_KINDS] */);
+
 #ifdef __cplusplus
 }
 #endif

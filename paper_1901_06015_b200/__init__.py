@@ -207,6 +207,13 @@ class ExecutionPlan(ctypes.Structure):
         return out
 
 
+class KernelStats(ctypes.Structure):
+    _fields_ = [("launches", c_uint64), ("total_ms", c_double), ("work", c_double)]
+
+
+KERNEL_KINDS = ("pack", "dmma", "ffma", "exact", "beta", "fill")
+
+
 def _round(v: float, prec: int) -> float:
     if prec == SINGLE:
         import struct
@@ -243,6 +250,9 @@ def _load() -> ctypes.CDLL:
         "mdg_rng_split_tag": (c_uint64, [c_uint64, c_char_p]),
         "mdg_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
         "mdg_shard_columns": (c_int, [c_int64, c_int32, c_int32, c_int64, POINTER(c_int64), POINTER(c_int64)]),
+        "mdg_launch_count": (c_uint64, []),
+        "mdg_profile_begin": (c_int, []),
+        "mdg_profile_end": (c_int, [POINTER(KernelStats)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -256,7 +266,25 @@ EXPORTED_SYMBOLS = (
     "mdg_config_validate", "mdg_view_make", "mdg_classify_case", "mdg_flops_of_case", "mdg_apply_scalar_policy",
     "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_async", "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
+    "mdg_launch_count", "mdg_profile_begin", "mdg_profile_end",
 )
+
+
+def launch_count() -> int:
+    """Kernels this process has launched through the library."""
+    return lib.mdg_launch_count()
+
+
+def profile_begin() -> None:
+    _check(lib.mdg_profile_begin())
+
+
+def profile_end() -> dict:
+    """{kind: {'launches', 'ms', 'work'}} for the kernels launched on this
+    thread since profile_begin(); work = flops (gemm) or bytes (pack/beta/fill)."""
+    out = (KernelStats * len(KERNEL_KINDS))()
+    _check(lib.mdg_profile_end(out))
+    return {k: {"launches": s.launches, "ms": s.total_ms, "work": s.work} for k, s in zip(KERNEL_KINDS, out)}
 
 
 def _check(rc: int) -> None:

@@ -4,6 +4,7 @@
 #include <exception>
 
 #include "driver.hpp"
+#include "profile.hpp"
 #include "mdgemm_b200.h"
 
 using namespace mdgemm;
@@ -310,6 +311,9 @@ int mdg_pack_operand(const mdg_view_t* src, int32_t side, int32_t format, int32_
 
 int mdg_fill_uniform(const mdg_view_t* v, uint64_t rng_state, void* stream) {
   return guarded([&] {
+    const MatrixView mv = view_from(v);
+    prof::Scope scope(MDG_KERNEL_FILL, static_cast<cudaStream_t>(stream),
+                      static_cast<double>(mv.m) * mv.n * dtype_size(mv.dtype));
     cuda_check(mdg::launch_fill_uniform(to_dview(view_from(v)), rng_state, static_cast<cudaStream_t>(stream)),
                "fill_uniform");
   });
@@ -332,6 +336,16 @@ int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align, int
     *j0 = lo;
     *nb = std::min<int64_t>(chunk, n - lo);
   });
+}
+
+uint64_t mdg_launch_count(void) { return prof::launches(); }
+
+int mdg_profile_begin(void) {
+  return guarded([&] { prof::begin(); });
+}
+
+int mdg_profile_end(mdg_kernel_stats_t* out) {
+  return guarded([&] { prof::end(out); });
 }
 
 }  // extern "C"

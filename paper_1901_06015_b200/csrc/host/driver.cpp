@@ -4,6 +4,7 @@
 // the pack kernels and one gemm kernel per call, and keeps the reference's
 // FlopCounter accounting.
 #include "driver.hpp"
+#include "profile.hpp"
 
 #include <algorithm>
 #include <mutex>
@@ -55,6 +56,12 @@ Packed prepare_pack(const MatrixView& src, Side side, PackFormat fmt, bool conj,
   Packed out;
   out.desc = make_pack_desc(src, side, fmt, conj, scale, target, halves ? tile / 2 : tile, lpad, &out.bytes);
   return out;
+}
+
+// Algorithmic bytes of one pack: the source elements read plus the packed
+// buffer written.
+double pack_traffic(const MatrixView& src, size_t packed) {
+  return static_cast<double>(src.m) * src.n * dtype_size(src.dtype) + static_cast<double>(packed);
 }
 
 bool onem_direct(const ExecutionPlan& p) {
@@ -161,7 +168,9 @@ mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format
 void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
                               Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
                               void* stream) {
-  const mdg::PackDesc d = make_pack_desc(src, side, format, conj, scale, target, reg_block, panel_len, nullptr);
+  size_t bytes = 0;
+  const mdg::PackDesc d = make_pack_desc(src, side, format, conj, scale, target, reg_block, panel_len, &bytes);
+  prof::Scope scope(MDG_KERNEL_PACK, static_cast<cudaStream_t>(stream), pack_traffic(src, bytes));
   cuda_check(mdg::launch_pack(d, dst, static_cast<cudaStream_t>(stream)), "pack kernel");
 }
 
@@ -174,8 +183,10 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (p.m == 0 || p.n == 0) return;
   if (p.k == 0) {
-    if (!p.beta.is_one())
+    if (!p.beta.is_one()) {
+      prof::Scope scope(MDG_KERNEL_BETA, st, 2.0 * p.c.m * p.c.n * dtype_size(p.c.dtype));
       cuda_check(mdg::launch_beta_pass(to_dview(p.c), to_dbeta(p.beta), st), "beta pass");
+    }
     return;
   }
   const bool single = p.comp_prec == Precision::Single;
@@ -193,8 +204,15 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   void* ws = nullptr;
   cuda_check(cudaMallocAsync(&ws, off_b + pb.bytes, st), "workspace allocation");
   char* wsa = static_cast<char*>(ws);
-  cudaError_t err = mdg::launch_pack(pa.desc, wsa, st);
-  if (err == cudaSuccess) err = mdg::launch_pack(pb.desc, wsa + off_b, st);
+  cudaError_t err;
+  {
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes));
+    err = mdg::launch_pack(pa.desc, wsa, st);
+  }
+  if (err == cudaSuccess) {
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, pb.bytes));
+    err = mdg::launch_pack(pb.desc, wsa + off_b, st);
+  }
 
   mdg::GemmDesc g{};
   g.a = mdg::DPanels{wsa, tile.bm, lpad};
@@ -229,8 +247,10 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
         g.exact_mode = mdg::EXACT_ONEM_MIXED;
         g.flat = to_dview(real_flatten(p.c, ax));
       }
+      prof::Scope scope(MDG_KERNEL_EXACT, st, 2.0 * p.m * p.n * p.k);
       err = mdg::launch_gemm_exact(g, single, st);
     } else {
+      prof::Scope scope(single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA, st, 2.0 * p.m * p.n * p.k);
       err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
     }
   }

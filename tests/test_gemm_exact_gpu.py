@@ -41,7 +41,7 @@ VARIANTS = [
     dict(c_kind="gen", trans_a=True, conj_a=True, conj_b=True),
 ]
 CONFIGS = [{}, {"ctemp.enable": "off", "gemm.kc": "8"}, {"ukr.preference": "row"},
-           {"ctemp.enable": "on", "gemm.threads": "3"}, {"gemm.kc": "6", "gemm.mc": "12", "gemm.nc": "12"}]
+           {"ctemp.enable": "on", "gemm.threads": "3"}, {"gemm.kc": "6", "gemm.mc": "16", "gemm.nc": "16"}]
 
 
 @pytest.mark.parametrize("label", ALL_LABELS[::2])

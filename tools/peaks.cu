@@ -40,7 +40,9 @@ __global__ void k_ffma(float* out, float s) {
 
 // m8n8k4: A 1 f64, B 1 f64, C 2 f64 per thread.
 __global__ void k_dmma_884(double* out) {
-  double a = threadIdx.x * 1e-3, b = 0.5;
+  double a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 1e-3 + i; b[i] = 0.5 + i; }
   double c[8][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0;
@@ -48,7 +50,7 @@ __global__ void k_dmma_884(double* out) {
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[i]), "d"(b[i]));
   }
   double r = 0;
 #pragma unroll
@@ -58,7 +60,9 @@ __global__ void k_dmma_884(double* out) {
 
 // m16n8k4: A 2, B 1, C 4.
 __global__ void k_dmma_1684(double* out) {
-  double a0 = threadIdx.x * 1e-3, a1 = 0.25, b = 0.5;
+  double a0[4], a1[4], b[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { a0[i] = threadIdx.x * 1e-3 + i; a1[i] = 0.25 * i; b[i] = 0.5 + i; }
   double c[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
@@ -66,7 +70,7 @@ __global__ void k_dmma_1684(double* out) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
-                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0), "d"(a1), "d"(b));
+                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3]) : "d"(a0[i]), "d"(a1[i]), "d"(b[i]));
   }
   double r = 0;
 #pragma unroll
