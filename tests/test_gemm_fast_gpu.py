@@ -77,11 +77,17 @@ def test_fast_larger_shapes(label):
 
 def test_beta_zero_never_reads_c():
     # acceptance.cpp:241-262: a C of all-ones bytes (NaN payloads) must not leak
-    for label in ("dddd", "zzzd", "sssd", "cdds", "sddd"):
+    for label in ("dddd", "zzzd", "sssd", "sddd", "cccs"):
         p = Problem(label, 16, 16, 16)
         p.C.buf[:] = 0xFF
         got, _ = run_fast(p, SCALARS["one"], SCALARS["zero"])
         assert np.all(np.isfinite(got.values()))
+    # case 1c updates Re(C) only: the poisoned Im(C) bits must come through untouched
+    p = Problem("cdds", 16, 16, 16)
+    p.C.buf[:] = 0xFF
+    got, _ = run_fast(p, SCALARS["one"], SCALARS["zero"])
+    assert np.all(np.isfinite(got.values().real))
+    assert np.all(got.values().imag.view(np.uint32) == 0xFFFFFFFF)
 
 
 def test_unread_imaginary_parts():
