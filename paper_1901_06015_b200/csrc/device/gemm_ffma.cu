@@ -8,6 +8,8 @@
 // threads each own an 8x8 register tile split into two 4x4 quadrants
 // ({ty*4, BM/2+ty*4} x {tx*4, BN/2+tx*4}) so every fragment is one
 // conflict-free LDS.128.  The fused typecast-accumulate epilogue follows.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mdg {
@@ -71,13 +73,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
   }
 
   // ------------------------------------------------------------ consumers
+  // acc[i][p] holds the column pair (2p, 2p+1) of register-tile row i; one
+  // FFMA2 (fma.rn.f32x2) updates a pair with A's element broadcast, so the
+  // 64 multiply-adds per inner step cost 32 issue slots.
   const int tx = tid % C::TXN, ty = tid / C::TXN;
   const int lane = tid & 31;
-  float acc[8][8];
+  uint64_t acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
 
   for (int kb = 0; kb < nk; ++kb) {
     const int s = kb % C::STAGES;
@@ -88,14 +93,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
     for (int kk = 0; kk < C::BK; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(a + kk * C::BM);
       const float4 a1 = *reinterpret_cast<const float4*>(a + kk * C::BM + C::BM / 2);
-      const float4 b0 = *reinterpret_cast<const float4*>(b + kk * C::BN);
-      const float4 b1 = *reinterpret_cast<const float4*>(b + kk * C::BN + C::BN / 2);
+      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN);
+      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN + C::BN / 2);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const uint64_t bp[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 8; ++i) {
+        uint64_t ai;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(ai) : "f"(av[i]));
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int p = 0; p < 4; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][p]) : "l"(ai), "l"(bp[p]));
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -104,13 +112,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
   // ------------------------------------------------------------ epilogue
   named_sync(1, C::NCT);
   float* T = reinterpret_cast<float*>(smem);  // BM x BN, column-major
+  auto lo = [](uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); };
+  auto hi = [](uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); };
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int c = (j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4));
-    *reinterpret_cast<float4*>(&T[c * C::BM + ty * 4]) =
-        make_float4(acc[0][j], acc[1][j], acc[2][j], acc[3][j]);
-    *reinterpret_cast<float4*>(&T[c * C::BM + C::BM / 2 + ty * 4]) =
-        make_float4(acc[4][j], acc[5][j], acc[6][j], acc[7][j]);
+    const int p = j >> 1;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (j & 1) ? hi(acc[i][p]) : lo(acc[i][p]);
+    *reinterpret_cast<float4*>(&T[c * C::BM + ty * 4]) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(&T[c * C::BM + C::BM / 2 + ty * 4]) = make_float4(v[4], v[5], v[6], v[7]);
   }
   named_sync(1, C::NCT);
   tile_epilogue(T, C::BM, C::BM, C::BN, static_cast<int64_t>(tm) * C::BM,
@@ -129,7 +141,16 @@ cudaError_t run(const GemmDesc& d, cudaStream_t s) {
 }
 
 using Big = FfmaCfg<128, 128, 4, 1>;
+using Big2 = FfmaCfg<128, 128, 4, 2>;  // 2 CTAs/SM (register-capped)
 using Small = FfmaCfg<64, 64, 4, 4>;
+
+int big_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("MDGEMM_FFMA_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 
 }  // namespace
 
@@ -140,7 +161,7 @@ FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms) {
 }
 
 cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s) {
-  if (t.bm == 128 && t.bn == 128) return run<Big>(d, s);
+  if (t.bm == 128 && t.bn == 128) return big_variant() == 2 ? run<Big2>(d, s) : run<Big>(d, s);
   if (t.bm == 64 && t.bn == 64) return run<Small>(d, s);
   return cudaErrorInvalidValue;
 }

@@ -38,6 +38,32 @@ __global__ void k_ffma(float* out, float s) {
   if (r == 1234.5f) out[0] = r;
 }
 
+// Paired fp32 FMA (sm_100 fma.rn.f32x2 -> SASS FFMA2), 3-register form with a
+// broadcast scalar operand, as the FFMA gemm mainloop issues it.
+__global__ void k_ffma2(float* out, float s) {
+  unsigned long long acc[8], x[8];
+  float bv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float v = threadIdx.x * 1e-3f + i;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc[i]) : "f"(v), "f"(v + 1.0f));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x[i]) : "f"(v * 0.5f), "f"(v * 0.25f));
+    bv[i] = s + i;
+  }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      unsigned long long b;
+      asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(bv[i]));
+      asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i]) : "l"(b), "l"(x[i]));
+    }
+  }
+  float r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r += __uint_as_float(static_cast<unsigned>(acc[i]));
+  if (r == 1234.5f) out[0] = r;
+}
+
 // m8n8k4: A 1 f64, B 1 f64, C 2 f64 per thread.
 __global__ void k_dmma_884(double* out) {
   double a[8], b[8];
@@ -154,6 +180,8 @@ int main(int argc, char** argv) {
     printf(", \"dfma_w%d_tflops\": %.3f", wpb, nthr * ITERS * 8 * 2 / (ms * 1e-3) / 1e12);
     ms = time_it([&] { k_ffma<<<grid, block>>>(fout, 0.999f); }, reps);
     printf(", \"ffma_w%d_tflops\": %.3f", wpb, nthr * ITERS * 16 * 2 / (ms * 1e-3) / 1e12);
+    ms = time_it([&] { k_ffma2<<<grid, block>>>(fout, 0.999f); }, reps);
+    printf(", \"ffma2_w%d_tflops\": %.3f", wpb, nthr * ITERS * 8 * 4 / (ms * 1e-3) / 1e12);
     double nwarps = double(grid.x) * wpb;
     ms = time_it([&] { k_dmma_884<<<grid, block>>>(dout); }, reps);
     printf(", \"dmma884_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 4) * 8 * (8 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
