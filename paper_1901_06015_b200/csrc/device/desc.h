@@ -78,6 +78,8 @@ struct GemmDesc {
   int64_t kc;          // EXACT_BLOCK_COMBINE block length (real inner steps)
   double seed_beta;    // EXACT_DIRECT_SEEDED: beta as passed to gemm_ukr
   DView flat;          // EXACT_ONEM_MIXED: real_flatten(C) of the 1m variant
+  int32_t group_rows;  // tile raster group height (0 = default 8)
+  int32_t reserved2;
 };
 
 // ---- host launchers (defined in the .cu files) ----

@@ -10,9 +10,12 @@
 //
 // Warp roles: warp NCW (last) is the producer (one elected lane issues the
 // bulk copies into a STAGES-deep ring); warps 0..NCW-1 consume.  After the
-// k loop the accumulator tile is staged through shared memory and every
-// compute thread runs the fused typecast-accumulate epilogue
-// (accumulate_element semantics, kernels.cpp:79-95) straight into C.
+// k loop the ring is reused for the fused typecast-accumulate epilogue
+// (fast_epilogue: accumulate_element semantics, kernels.cpp:79-95), which
+// moves C through shared memory with TMA bulk copies.  The kernel is
+// instantiated per C storage datatype (CDT) so the epilogue stays small.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mdg {
@@ -28,8 +31,11 @@ struct DmmaCfg {
   static constexpr int MT = WTM / 8, NT = WTN / 8;
   static constexpr int STAGE_A = BK * BM, STAGE_B = BK * BN;  // doubles
   static constexpr size_t RING_BYTES = size_t(STAGES) * (STAGE_A + STAGE_B) * sizeof(double);
-  static constexpr size_t SMEM = RING_BYTES + 2 * STAGES * sizeof(uint64_t);
-  static_assert(size_t(BM) * BN * sizeof(double) <= RING_BYTES, "epilogue tile must fit the ring");
+  // epilogue: the staged accumulator tile (<= 8 bytes per real element) plus
+  // C chunks of at least half the tile
+  static constexpr size_t EPI_BYTES = size_t(BM) * BN * sizeof(double) * 3 / 2;
+  static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
+  static constexpr size_t SMEM = REGION + (2 * STAGES + 1) * sizeof(uint64_t);
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
 };
 
@@ -39,18 +45,19 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <class C>
+template <class C, int CDT>
 __global__ void __launch_bounds__(C::THREADS, 1) gemm_dmma_kernel(GemmDesc d) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = sA + C::STAGES * C::STAGE_A;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::REGION);
   uint64_t* empty = full + C::STAGES;
+  uint64_t* cbar = empty + C::STAGES;  // C-chunk load completion
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
   int tm, tn;
-  tile_coords(blockIdx.x, tiles_m, tiles_n, tm, tn);
+  tile_coords(blockIdx.x, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
   const int nk = static_cast<int>(lpad / C::BK);
   const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
@@ -62,6 +69,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) gemm_dmma_kernel(GemmDesc d) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
+    mbar_init(cbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -114,29 +122,31 @@ __global__ void __launch_bounds__(C::THREADS, 1) gemm_dmma_kernel(GemmDesc d) {
   // ------------------------------------------------------------ epilogue
   constexpr int NCT = C::NCW * 32;
   named_sync(1, NCT);  // every consumer is done with the ring
-  double* T = reinterpret_cast<double*>(smem);  // BM x BN, column-major
+  fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
+                     static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, threadIdx.x, NCT, [&](auto&& put) {
 #pragma unroll
-  for (int i = 0; i < C::MT; ++i)
+                       for (int i = 0; i < C::MT; ++i)
 #pragma unroll
-    for (int j = 0; j < C::NT; ++j) {
-      const int r = wm * C::WTM + i * 8 + g;
-      const int c = wn * C::WTN + j * 8 + 2 * tig;
-      T[c * C::BM + r] = acc[i][j][0];
-      T[(c + 1) * C::BM + r] = acc[i][j][1];
-    }
-  named_sync(1, NCT);
-  tile_epilogue(T, C::BM, C::BM, C::BN, static_cast<int64_t>(tm) * C::BM,
-                static_cast<int64_t>(tn) * C::BN, d.epi, threadIdx.x, NCT);
+                         for (int j = 0; j < C::NT; ++j) {
+                           const int r = wm * C::WTM + i * 8 + g;
+                           const int c = wn * C::WTN + j * 8 + 2 * tig;
+                           put(r, c, acc[i][j][0]);
+                           put(r, c + 1, acc[i][j][1]);
+                         }
+                     });
 }
 
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_dmma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(C::SMEM));
-  if (e != cudaSuccess) return e;
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
-  gemm_dmma_kernel<C><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+  cudaError_t e = cudaSuccess;
+  MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
+    e = cudaFuncSetAttribute(gemm_dmma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::SMEM));
+    if (e != cudaSuccess) return e;
+    gemm_dmma_kernel<C, CDT><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+  });
   return cudaGetLastError();
 }
 
@@ -146,6 +156,10 @@ using Small = DmmaCfg<64, 64, 2, 2, 4>;
 }  // namespace
 
 FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms) {
+  if (const char* force = std::getenv("MDGEMM_DMMA_TILE")) {  // tuning override
+    const int t = std::atoi(force);
+    if (t == 64 || t == 128) return FastTile{t, t, 16};
+  }
   const int64_t big = ((me + 127) / 128) * ((ne + 127) / 128);
   if (big >= 4LL * sms) return FastTile{128, 128, 16};
   const int64_t small = ((me + 63) / 64) * ((ne + 63) / 64);

@@ -1,13 +1,17 @@
 // FAST numerics, computation precision single: the reference's float
-// microkernel (ukr_impl<float>, kernels.cpp:7-40) as an FP32 FFMA SIMT CTA
-// tile.  No TF32: tensor cores would not reproduce fp32 products.
+// microkernel (ukr_impl<float>, kernels.cpp:7-40) as an FP32 SIMT CTA tile.
+// No TF32: tensor cores would not reproduce fp32 products.
 //
 // Same feed as the DMMA kernel: a producer warp streams BK x BM / BK x BN
 // slabs of the packed panels into a STAGES-deep shared-memory ring with one
-// TMA bulk copy per operand per stage (mbarrier completion); the compute
-// threads each own an 8x8 register tile split into two 4x4 quadrants
+// TMA bulk copy per operand per stage (mbarrier completion).  Each compute
+// thread owns an 8x8 register tile split into two 4x4 quadrants
 // ({ty*4, BM/2+ty*4} x {tx*4, BN/2+tx*4}) so every fragment is one
-// conflict-free LDS.128.  The fused typecast-accumulate epilogue follows.
+// conflict-free LDS.128, and updates it with Blackwell's paired FP32 FMA
+// (fma.rn.f32x2 -> SASS FFMA2, A's element broadcast into both lanes), which
+// halves the issue slots of the outer product.  The fused typecast-accumulate
+// epilogue (fast_epilogue) follows; the kernel is instantiated per C
+// storage datatype.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -25,23 +29,27 @@ struct FfmaCfg {
   static constexpr int THREADS = NCT + 32;
   static constexpr int STAGE_A = BK * BM, STAGE_B = BK * BN;  // floats
   static constexpr size_t RING_BYTES = size_t(STAGES) * (STAGE_A + STAGE_B) * sizeof(float);
-  static constexpr size_t SMEM = RING_BYTES + 2 * STAGES * sizeof(uint64_t);
+  // epilogue: the staged accumulator tile (<= 8 bytes per real element) plus
+  // C chunks of at least half the tile
+  static constexpr size_t EPI_BYTES = size_t(BM) * BN * sizeof(double) * 3 / 2;
+  static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
+  static constexpr size_t SMEM = REGION + (2 * STAGES + 1) * sizeof(uint64_t);
   static_assert(NCT % 32 == 0, "compute threads must be whole warps");
-  static_assert(size_t(BM) * BN * sizeof(float) <= RING_BYTES, "epilogue tile must fit the ring");
 };
 
-template <class C>
+template <class C, int CDT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc d) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* sA = reinterpret_cast<float*>(smem);
   float* sB = sA + C::STAGES * C::STAGE_A;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::REGION);
   uint64_t* empty = full + C::STAGES;
+  uint64_t* cbar = empty + C::STAGES;  // C-chunk load completion
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
   int tm, tn;
-  tile_coords(blockIdx.x, tiles_m, tiles_n, tm, tn);
+  tile_coords(blockIdx.x, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
   const int nk = static_cast<int>(lpad / C::BK);
   const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
@@ -53,6 +61,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
+    mbar_init(cbar, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -74,8 +83,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
 
   // ------------------------------------------------------------ consumers
   // acc[i][p] holds the column pair (2p, 2p+1) of register-tile row i; one
-  // FFMA2 (fma.rn.f32x2) updates a pair with A's element broadcast, so the
-  // 64 multiply-adds per inner step cost 32 issue slots.
+  // FFMA2 updates a pair with A's element broadcast, so the 64 multiply-adds
+  // per inner step cost 32 issue slots.
   const int tx = tid % C::TXN, ty = tid / C::TXN;
   const int lane = tid & 31;
   uint64_t acc[8][4];
@@ -110,47 +119,38 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
   }
 
   // ------------------------------------------------------------ epilogue
-  named_sync(1, C::NCT);
-  float* T = reinterpret_cast<float*>(smem);  // BM x BN, column-major
-  auto lo = [](uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v)); };
-  auto hi = [](uint64_t v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); };
+  named_sync(1, C::NCT);  // every consumer is done with the ring
+  fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
+                     static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, tid, C::NCT, [&](auto&& put) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const int c = (j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4));
-    const int p = j >> 1;
-    float v[8];
+                       for (int i = 0; i < 8; ++i) {
+                         const int r = i < 4 ? ty * 4 + i : C::BM / 2 + ty * 4 + (i - 4);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = (j & 1) ? hi(acc[i][p]) : lo(acc[i][p]);
-    *reinterpret_cast<float4*>(&T[c * C::BM + ty * 4]) = make_float4(v[0], v[1], v[2], v[3]);
-    *reinterpret_cast<float4*>(&T[c * C::BM + C::BM / 2 + ty * 4]) = make_float4(v[4], v[5], v[6], v[7]);
-  }
-  named_sync(1, C::NCT);
-  tile_epilogue(T, C::BM, C::BM, C::BN, static_cast<int64_t>(tm) * C::BM,
-                static_cast<int64_t>(tn) * C::BN, d.epi, tid, C::NCT);
+                         for (int j = 0; j < 8; ++j) {
+                           const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
+                           const uint64_t v = acc[i][j >> 1];
+                           put(r, c, __uint_as_float(static_cast<uint32_t>((j & 1) ? (v >> 32) : v)));
+                         }
+                       }
+                     });
 }
 
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(gemm_ffma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(C::SMEM));
-  if (e != cudaSuccess) return e;
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
-  gemm_ffma_kernel<C><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+  cudaError_t e = cudaSuccess;
+  MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
+    e = cudaFuncSetAttribute(gemm_ffma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::SMEM));
+    if (e != cudaSuccess) return e;
+    gemm_ffma_kernel<C, CDT><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+  });
   return cudaGetLastError();
 }
 
 using Big = FfmaCfg<128, 128, 4, 1>;
-using Big2 = FfmaCfg<128, 128, 4, 2>;  // 2 CTAs/SM (register-capped)
 using Small = FfmaCfg<64, 64, 4, 4>;
-
-int big_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("MDGEMM_FFMA_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  return v;
-}
 
 }  // namespace
 
@@ -161,7 +161,7 @@ FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms) {
 }
 
 cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s) {
-  if (t.bm == 128 && t.bn == 128) return big_variant() == 2 ? run<Big2>(d, s) : run<Big>(d, s);
+  if (t.bm == 128 && t.bn == 128) return run<Big>(d, s);
   if (t.bm == 64 && t.bn == 64) return run<Small>(d, s);
   return cudaErrorInvalidValue;
 }

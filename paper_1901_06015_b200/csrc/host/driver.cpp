@@ -7,6 +7,7 @@
 #include "profile.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -227,6 +228,11 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   g.epi.ne = p.n;
   g.kc = p.params.kc;
   g.seed_beta = p.beta.re;
+  // Short inner dimension: C traffic dominates, walk whole tile-columns so the
+  // concurrently written C stays within a few column panels (TLB reach);
+  // otherwise 8-row groups for A/B panel reuse in L2.
+  g.group_rows = p.k <= 512 ? static_cast<int32_t>((p.m + tile.bm - 1) / tile.bm) : 8;
+  if (const char* force = std::getenv("MDGEMM_GROUP_ROWS")) g.group_rows = std::atoi(force);
 
   if (err == cudaSuccess) {
     if (exact) {
