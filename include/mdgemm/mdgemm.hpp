@@ -268,6 +268,19 @@ ExecutionPlan plan(Scalar alpha, const MatrixView& a, const MatrixView& b, Scala
 void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,
           const MatrixView& c, const Config& cfg = Config::defaults(), FlopCounter* fc = nullptr);
 
+// A list of independent gemm() calls, equivalent to calling gemm() on each in
+// order, with the host-operand staging of one call overlapped with the
+// kernels of its neighbours (copy-in / compute / copy-out streams).
+// Synchronous.  B200 extension.
+struct GemmCall {
+  Scalar alpha;
+  MatrixView a, b;
+  Scalar beta;
+  MatrixView c;
+};
+void gemm_batch(const std::vector<GemmCall>& calls, const Config& cfg = Config::defaults(),
+                FlopCounter* fc = nullptr);
+
 // Device-pointer variant ordered on `stream` (a cudaStream_t); returns
 // without synchronising.
 void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,

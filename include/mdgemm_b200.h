@@ -170,6 +170,19 @@ int mdg_gemm(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b,
              mdg_scalar_t beta, const mdg_view_t* c, const mdg_config_t* cfg,
              uint64_t* flops_out);
 
+/* A batch of independent gemm() calls, equivalent to mdg_gemm on each in
+ * order; host operands are staged with copy-in / compute / copy-out
+ * pipelined across calls.  Synchronous. */
+typedef struct mdg_gemm_call {
+  mdg_scalar_t alpha;
+  mdg_view_t a, b;
+  mdg_scalar_t beta;
+  mdg_view_t c;
+} mdg_gemm_call_t;
+
+int mdg_gemm_batch(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg,
+                   uint64_t* flops_out);
+
 /* Same with device pointers only, stream-ordered, no synchronisation. */
 int mdg_gemm_async(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b,
                    mdg_scalar_t beta, const mdg_view_t* c, const mdg_config_t* cfg,

@@ -17,7 +17,7 @@ from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, 
 
 __all__ = [
     "Error", "ScalarPolicyError", "CudaError", "lib", "MatrixView", "Scalar", "Config", "ExecutionPlan",
-    "plan", "gemm", "gemm_async", "execute", "pack_block_device", "packed_bytes", "fill_uniform",
+    "plan", "gemm", "gemm_batch", "gemm_async", "execute", "pack_block_device", "packed_bytes", "fill_uniform",
     "Rng", "classify_case", "flops_of_case", "apply_scalar_policy", "shard_columns", "CaseLabel",
     "DT_S", "DT_D", "DT_C", "DT_Z", "SINGLE", "DOUBLE", "LEFT", "RIGHT", "STANDARD", "ONE_E", "ONE_R",
     "FAST", "EXACT", "dtype_from_letter", "dtype_letter", "dtype_size", "is_complex", "precision_of",
@@ -207,6 +207,11 @@ class ExecutionPlan(ctypes.Structure):
         return out
 
 
+class GemmCall(ctypes.Structure):
+    """One element of gemm_batch(): C := beta*C + alpha*A*B."""
+    _fields_ = [("alpha", Scalar), ("a", MatrixView), ("b", MatrixView), ("beta", Scalar), ("c", MatrixView)]
+
+
 class KernelStats(ctypes.Structure):
     _fields_ = [("launches", c_uint64), ("total_ms", c_double), ("work", c_double)]
 
@@ -244,6 +249,7 @@ def _load() -> ctypes.CDLL:
         "mdg_execute": (c_int, [P, c_int32, c_void_p, POINTER(c_uint64)]),
         "mdg_gemm": (c_int, [S, V, V, S, V, C, POINTER(c_uint64)]),
         "mdg_gemm_async": (c_int, [S, V, V, S, V, C, c_void_p, POINTER(c_uint64)]),
+        "mdg_gemm_batch": (c_int, [c_int32, POINTER(GemmCall), C, POINTER(c_uint64)]),
         "mdg_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64, c_int64]),
         "mdg_pack_operand": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
         "mdg_fill_uniform": (c_int, [V, c_uint64, c_void_p]),
@@ -264,7 +270,7 @@ lib = _load()
 EXPORTED_SYMBOLS = (
     "mdg_abi_version", "mdg_last_error", "mdg_config_defaults", "mdg_config_set", "mdg_config_load",
     "mdg_config_validate", "mdg_view_make", "mdg_classify_case", "mdg_flops_of_case", "mdg_apply_scalar_policy",
-    "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_async", "mdg_packed_bytes", "mdg_pack_operand",
+    "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_async", "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
     "mdg_launch_count", "mdg_profile_begin", "mdg_profile_end",
 )
@@ -333,6 +339,15 @@ def gemm(alpha: Scalar, a: MatrixView, b: MatrixView, beta: Scalar, c: MatrixVie
     """C := beta*C + alpha*A*B (dispatch.hpp:89-91).  Synchronous; returns the FlopCounter value."""
     flops = c_uint64(0)
     _check(lib.mdg_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(flops)))
+    return flops.value
+
+
+def gemm_batch(calls, cfg: Config | None = None) -> int:
+    """Independent gemm() calls [(alpha, a, b, beta, c), ...] in order, with host
+    operand staging pipelined across calls.  Synchronous; returns the FlopCounter total."""
+    arr = (GemmCall * max(len(calls), 1))(*[GemmCall(al, a, b, be, c) for al, a, b, be, c in calls])
+    flops = c_uint64(0)
+    _check(lib.mdg_gemm_batch(len(calls), arr, byref(cfg or Config.defaults()), byref(flops)))
     return flops.value
 
 

@@ -266,92 +266,4 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   if (fc) fc->add(reference_flops(p));
 }
 
-// ----------------------------------------------------------------- gemm()
-
-namespace {
-
-bool is_device_ptr(const void* ptr) {
-  if (!ptr) return false;
-  cudaPointerAttributes attr{};
-  if (cudaPointerGetAttributes(&attr, ptr) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
-}
-
-struct Staged {
-  const std::byte* lo = nullptr;
-  const std::byte* hi = nullptr;
-  std::byte* dev = nullptr;
-};
-
-}  // namespace
-
-void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
-                const Config& cfg, void* stream, FlopCounter* fc) {
-  if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
-  const ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
-  execute(p, cfg.numerics, stream, fc);
-}
-
-void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
-          const Config& cfg, FlopCounter* fc) {
-  if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
-  ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
-  cudaStream_t st = cudaStreamPerThread;
-  if (p.m == 0 || p.n == 0) return;
-
-  // Host operands are staged through HBM: copy each operand's byte window,
-  // rebase the plan's views into the copies, copy C's window back.
-  const MatrixView* originals[3] = {&a, &b, &c};
-  const bool need[3] = {p.k > 0, p.k > 0, true};
-  Staged stg[3];
-  bool any_host = false;
-  for (int i = 0; i < 3; ++i) {
-    const auto [lo, hi] = byte_range(*originals[i]);
-    stg[i].lo = lo;
-    stg[i].hi = hi;
-    if (need[i] && hi > lo && !is_device_ptr(lo)) any_host = true;
-  }
-  std::vector<void*> allocations;
-  auto release = [&] {
-    for (void* q : allocations) cudaFreeAsync(q, st);
-    cudaStreamSynchronize(st);
-  };
-  try {
-    if (any_host) {
-      for (int i = 0; i < 3; ++i) {
-        if (!need[i] || stg[i].hi <= stg[i].lo || is_device_ptr(stg[i].lo)) continue;
-        const size_t bytes = static_cast<size_t>(stg[i].hi - stg[i].lo);
-        void* d = nullptr;
-        cuda_check(cudaMallocAsync(&d, bytes, st), "staging allocation");
-        allocations.push_back(d);
-        stg[i].dev = static_cast<std::byte*>(d);
-        cuda_check(cudaMemcpyAsync(d, stg[i].lo, bytes, cudaMemcpyHostToDevice, st), "H2D staging");
-      }
-      auto rebase = [&](MatrixView& v) {
-        for (int i = 0; i < 3; ++i)
-          if (stg[i].dev && v.base >= stg[i].lo && v.base < stg[i].hi) {
-            v.base = stg[i].dev + (v.base - stg[i].lo);
-            return;
-          }
-      };
-      rebase(p.a);
-      rebase(p.b);
-      rebase(p.c);
-    }
-    execute(p, cfg.numerics, st, fc);
-    if (stg[2].dev)
-      cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(stg[2].lo), stg[2].dev,
-                                 static_cast<size_t>(stg[2].hi - stg[2].lo), cudaMemcpyDeviceToHost, st),
-                 "D2H staging");
-    cuda_check(cudaStreamSynchronize(st), "gemm synchronisation");
-  } catch (...) {
-    release();
-    throw;
-  }
-  release();
-}
-
 }  // namespace mdgemm
