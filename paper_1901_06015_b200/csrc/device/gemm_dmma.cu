@@ -21,9 +21,9 @@
 namespace mdg {
 namespace {
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1>
 struct DmmaCfg {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   static constexpr int BK = 16;
   static constexpr int NCW = WM * WN;
   static constexpr int THREADS = (NCW + 1) * 32;
@@ -46,7 +46,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 template <class C, int CDT>
-__global__ void __launch_bounds__(C::THREADS, 1) gemm_dmma_kernel(GemmDesc d) {
+__global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc d) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = sA + C::STAGES * C::STAGE_A;
@@ -151,27 +151,32 @@ cudaError_t run(const GemmDesc& d, cudaStream_t s) {
 }
 
 using Big = DmmaCfg<128, 128, 2, 4, 4>;
+// Two CTAs per SM (4 DMMA warps each, same 64x32 warp tiles): one CTA's
+// epilogue overlaps the other's mainloop.
+using Pair = DmmaCfg<64, 128, 1, 4, 4, 2>;
 using Small = DmmaCfg<64, 64, 2, 2, 4>;
 
 }  // namespace
 
 FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms) {
-  if (const char* force = std::getenv("MDGEMM_DMMA_TILE")) {  // tuning override
+  if (const char* force = std::getenv("MDGEMM_DMMA_TILE")) {  // tuning override: 64 | 128 | 64128
     const int t = std::atoi(force);
     if (t == 64 || t == 128) return FastTile{t, t, 16};
+    if (t == 64128) return FastTile{64, 128, 16};
   }
-  const int64_t big = ((me + 127) / 128) * ((ne + 127) / 128);
-  if (big >= 4LL * sms) return FastTile{128, 128, 16};
+  // 64x128 tiles, two CTAs per SM (measured better than 128x128 at every
+  // BASELINE shape), once they fill the machine evenly; 64x64 (three per SM)
+  // for small problems.
+  const int64_t pair = ((me + 63) / 64) * ((ne + 127) / 128);
   const int64_t small = ((me + 63) / 64) * ((ne + 63) / 64);
-  // 3 small CTAs fit per SM; prefer the big tile once it fills the machine
-  // about as evenly as the small one does.
-  const double eff_big = double(big) / (double((big + sms - 1) / sms) * sms);
+  const double eff_pair = double(pair) / (double((pair + 2 * sms - 1) / (2 * sms)) * 2 * sms);
   const double eff_small = double(small) / (double((small + 3 * sms - 1) / (3 * sms)) * 3 * sms);
-  return eff_big >= 0.9 * eff_small && big >= sms ? FastTile{128, 128, 16} : FastTile{64, 64, 16};
+  return pair >= 2LL * sms && eff_pair >= 0.9 * eff_small ? FastTile{64, 128, 16} : FastTile{64, 64, 16};
 }
 
 cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s) {
   if (t.bm == 128 && t.bn == 128) return run<Big>(d, s);
+  if (t.bm == 64 && t.bn == 128) return run<Pair>(d, s);
   if (t.bm == 64 && t.bn == 64) return run<Small>(d, s);
   return cudaErrorInvalidValue;
 }
