@@ -54,7 +54,8 @@ def parse_args():
     ap.add_argument("--workload", default="sweep",
                     choices=["sweep", "cfg1", "cfg3", "cfg4-cdds", "cfg4-szzs", "cfg4-zczd",
                              "cfg5-k64", "cfg5-k256", "cfg5-k1024"])
-    ap.add_argument("--size", type=int, default=4096, help="sweep size m=n=k")
+    ap.add_argument("--size", type=int, default=0, help="run the sweep at this single size m=n=k")
+    ap.add_argument("--sizes", default="256:4096:256", help="sweep sizes lo:hi:step (BASELINE configs[1])")
     ap.add_argument("--labels", default="", help="comma-separated subset of labels (sweep)")
     ap.add_argument("--numerics", choices=["fast", "exact"], default="fast")
     ap.add_argument("--no-e2e", action="store_true")
@@ -73,13 +74,20 @@ def workload(args):
         labels = [l.str() for l in M.CaseLabel.all()]
         if args.labels:
             labels = [l for l in args.labels.split(",") if l]
+        if args.size:
+            sizes = [args.size]
+        else:
+            lo, hi, st = (int(x) for x in args.sizes.split(":"))
+            sizes = list(range(lo, hi + 1, st))
         items = []
-        for lab in labels:
-            cid = M.CaseLabel.parse(lab).case_id()
-            alpha = S.complex_value(1.2, -0.7) if cid in (0, 7) else S.real_value(1.2)
-            items.append((lab, args.size, args.size, args.size, alpha, S.complex_value(0.9, 0.3)))
-        desc = (f"BASELINE configs[1]: {len(labels)}-label sweep at m=n=k={args.size}, column-major, "
-                "alpha=1.2-0.7i (cases 0,3; real 1.2 otherwise), beta=0.9+0.3i")
+        for s in sizes:
+            for lab in labels:
+                cid = M.CaseLabel.parse(lab).case_id()
+                alpha = S.complex_value(1.2, -0.7) if cid in (0, 7) else S.real_value(1.2)
+                items.append((lab, s, s, s, alpha, S.complex_value(0.9, 0.3)))
+        span = f"m=n=k={sizes[0]}" if len(sizes) == 1 else f"m=n=k={sizes[0]}..{sizes[-1]} step {sizes[1] - sizes[0]}"
+        desc = (f"BASELINE configs[1]: {len(labels)}-label sweep, {span} ({len(items)} gemm calls per step), "
+                "column-major, alpha=1.2-0.7i (cases 0,3; real 1.2 otherwise), beta=0.9+0.3i")
         return desc, items, "uniform"
     if args.workload == "cfg1":
         return ("BASELINE configs[0]: dssd m=n=k=1024, alpha=beta=1",
@@ -357,7 +365,11 @@ def reference_sample(args):
     desc, items, _ = workload(args)
     if args.workload == "sweep":
         s = args.cpu_size
-        sample = [(l, s, s, s, al, be) for l, _, _, _, al, be in items]
+        seen, sample = set(), []
+        for l, _, _, _, al, be in items:
+            if l not in seen:
+                seen.add(l)
+                sample.append((l, s, s, s, al, be))
         text = f"all {len(sample)} sweep labels at m=n=k={s}"
     else:
         sample, text = [], ""

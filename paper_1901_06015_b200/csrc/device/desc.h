@@ -57,6 +57,8 @@ struct PackDesc {
   int64_t len;             // logical panel length
   int64_t lpad;            // allocated panel length (>= len), zero-filled
   int64_t ext_i, ext_j;    // source index space incl. panel padding
+  int32_t pd_shift;        // log2(pd) when pd is a power of two, else -1
+  int32_t reserved;
 };
 
 // Exact (reference-replaying) gemm modes.

@@ -85,10 +85,13 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_kernel(PackDesc d, D* __res
     const int64_t i = i0 + ii, j = j0 + jj;
     if (i >= d.ext_i || j >= d.ext_j) continue;
     const double2 v = tile[jj][ii];
-    // offset of packed-logical (pr, pc) in block elements
+    // offset of packed-logical (pr, pc) in block elements; power-of-two panel
+    // dims (every kernel tile) avoid the 64-bit division per element
+    const int sh = d.pd_shift;
     auto off = [&](int64_t pr, int64_t pc) -> int64_t {
-      return SIDE == MDG_SIDE_LEFT ? (pr / PD) * PD * LP + pc * PD + pr % PD
-                                   : (pc / PD) * PD * LP + pr * PD + pc % PD;
+      const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
+      if (sh >= 0) return ((x >> sh) * LP + y) * PD + (x & (PD - 1));
+      return (x / PD) * PD * LP + y * PD + x % PD;
     };
     if constexpr (FMT == MDG_FMT_STANDARD) {
       if constexpr (SRC_COMPLEX) {

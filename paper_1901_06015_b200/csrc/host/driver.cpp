@@ -155,6 +155,10 @@ mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format
   d.target_single = target.precision == Precision::Single;
   d.out_complex = g.block_dtype.domain == Domain::Complex;
   d.pd = reg_block;
+  d.pd_shift = -1;
+  if ((reg_block & (reg_block - 1)) == 0)
+    for (int s = 0; s < 63; ++s)
+      if ((int64_t{1} << s) == reg_block) d.pd_shift = s;
   d.panels = g.panels;
   d.len = g.len;
   d.lpad = g.lpad;
