@@ -221,8 +221,9 @@ def run_b200(args):
         if world > 1:
             for t in a_bufs:
                 dist.broadcast(t, src=0)
-        for al, va, vb, be, vc in calls:
-            M.gemm_async(al, va, vb, be, vc, cfg, stream)
+        # the step's calls as one batch, forked from / joined into the timed stream: calls that
+        # share no memory (different C buffers) run concurrently on the library's compute streams
+        M.gemm_batch(calls, cfg, stream=stream, sync=False)
 
     for _ in range(args.warmup):
         step()

@@ -280,6 +280,10 @@ struct GemmCall {
 };
 void gemm_batch(const std::vector<GemmCall>& calls, const Config& cfg = Config::defaults(),
                 FlopCounter* fc = nullptr);
+// Same, forked from and joined back into `stream` (a cudaStream_t) without
+// synchronising; host operands must stay valid until the stream completes.
+void gemm_batch_async(const std::vector<GemmCall>& calls, const Config& cfg, void* stream,
+                      FlopCounter* fc = nullptr);
 
 // Device-pointer variant ordered on `stream` (a cudaStream_t); returns
 // without synchronising.

@@ -183,6 +183,11 @@ typedef struct mdg_gemm_call {
 int mdg_gemm_batch(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg,
                    uint64_t* flops_out);
 
+/* Same, forked from and joined back into `stream` without synchronising
+ * (independent calls run concurrently on the library's compute streams). */
+int mdg_gemm_batch_async(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg,
+                         void* stream, uint64_t* flops_out);
+
 /* Same with device pointers only, stream-ordered, no synchronisation. */
 int mdg_gemm_async(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b,
                    mdg_scalar_t beta, const mdg_view_t* c, const mdg_config_t* cfg,

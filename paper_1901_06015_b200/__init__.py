@@ -250,6 +250,7 @@ def _load() -> ctypes.CDLL:
         "mdg_gemm": (c_int, [S, V, V, S, V, C, POINTER(c_uint64)]),
         "mdg_gemm_async": (c_int, [S, V, V, S, V, C, c_void_p, POINTER(c_uint64)]),
         "mdg_gemm_batch": (c_int, [c_int32, POINTER(GemmCall), C, POINTER(c_uint64)]),
+        "mdg_gemm_batch_async": (c_int, [c_int32, POINTER(GemmCall), C, c_void_p, POINTER(c_uint64)]),
         "mdg_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64, c_int64]),
         "mdg_pack_operand": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
         "mdg_fill_uniform": (c_int, [V, c_uint64, c_void_p]),
@@ -270,7 +271,8 @@ lib = _load()
 EXPORTED_SYMBOLS = (
     "mdg_abi_version", "mdg_last_error", "mdg_config_defaults", "mdg_config_set", "mdg_config_load",
     "mdg_config_validate", "mdg_view_make", "mdg_classify_case", "mdg_flops_of_case", "mdg_apply_scalar_policy",
-    "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_async", "mdg_packed_bytes", "mdg_pack_operand",
+    "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_batch_async", "mdg_gemm_async",
+    "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
     "mdg_launch_count", "mdg_profile_begin", "mdg_profile_end",
 )
@@ -342,12 +344,18 @@ def gemm(alpha: Scalar, a: MatrixView, b: MatrixView, beta: Scalar, c: MatrixVie
     return flops.value
 
 
-def gemm_batch(calls, cfg: Config | None = None) -> int:
-    """Independent gemm() calls [(alpha, a, b, beta, c), ...] in order, with host
-    operand staging pipelined across calls.  Synchronous; returns the FlopCounter total."""
+def gemm_batch(calls, cfg: Config | None = None, stream=None, sync: bool = True) -> int:
+    """gemm() calls [(alpha, a, b, beta, c), ...] with the semantics of calling
+    them in order; host staging is pipelined and calls that do not touch each
+    other's memory run concurrently.  sync=False forks from / joins into
+    `stream` without waiting.  Returns the FlopCounter total."""
     arr = (GemmCall * max(len(calls), 1))(*[GemmCall(al, a, b, be, c) for al, a, b, be, c in calls])
     flops = c_uint64(0)
-    _check(lib.mdg_gemm_batch(len(calls), arr, byref(cfg or Config.defaults()), byref(flops)))
+    if sync:
+        _check(lib.mdg_gemm_batch(len(calls), arr, byref(cfg or Config.defaults()), byref(flops)))
+    else:
+        _check(lib.mdg_gemm_batch_async(len(calls), arr, byref(cfg or Config.defaults()), _stream_ptr(stream),
+                                        byref(flops)))
     return flops.value
 
 

@@ -280,16 +280,29 @@ int mdg_gemm(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b, mdg_s
   });
 }
 
+static std::vector<GemmCall> call_list(int32_t count, const mdg_gemm_call_t* calls) {
+  if (count < 0 || (count > 0 && !calls)) throw Error("mdg_gemm_batch: bad call list");
+  std::vector<GemmCall> list;
+  list.reserve(static_cast<size_t>(count));
+  for (int32_t i = 0; i < count; ++i)
+    list.push_back(GemmCall{scalar_from(calls[i].alpha), view_from(&calls[i].a), view_from(&calls[i].b),
+                            scalar_from(calls[i].beta), view_from(&calls[i].c)});
+  return list;
+}
+
 int mdg_gemm_batch(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg, uint64_t* flops_out) {
   return guarded([&] {
-    if (count < 0 || (count > 0 && !calls)) throw Error("mdg_gemm_batch: bad call list");
-    std::vector<GemmCall> list;
-    list.reserve(static_cast<size_t>(count));
-    for (int32_t i = 0; i < count; ++i)
-      list.push_back(GemmCall{scalar_from(calls[i].alpha), view_from(&calls[i].a), view_from(&calls[i].b),
-                              scalar_from(calls[i].beta), view_from(&calls[i].c)});
     FlopCounter fc;
-    gemm_batch(list, config_from(cfg), &fc);
+    gemm_batch(call_list(count, calls), config_from(cfg), &fc);
+    if (flops_out) *flops_out = fc.value();
+  });
+}
+
+int mdg_gemm_batch_async(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg, void* stream,
+                         uint64_t* flops_out) {
+  return guarded([&] {
+    FlopCounter fc;
+    gemm_batch_async(call_list(count, calls), config_from(cfg), stream, &fc);
     if (flops_out) *flops_out = fc.value();
   });
 }

@@ -3,12 +3,18 @@
 // host Matrix objects): each host operand's byte window is copied into HBM,
 // the plan's views are rebased into the copy, and C's window is copied back.
 //
-// gemm_batch() runs a list of independent gemm calls with the host staging
-// pipelined across calls on three streams -- copy-in, compute, copy-out --
-// so the PCIe transfers of one call overlap the kernels of its neighbours.
-// Ordering is that of calling gemm() on each element in turn: a call whose
-// host inputs overlap an earlier call's host output waits for that copy-out;
-// device-resident operands are ordered by the single compute stream.
+// gemm_batch() runs a list of gemm calls with the semantics of calling gemm()
+// on each in order, but
+//   * host staging is pipelined across calls (copy-in / compute / copy-out
+//     streams), so one call's PCIe traffic overlaps its neighbours' kernels;
+//   * calls that do not touch each other's memory run concurrently on
+//     several compute streams, so small problems share the GPU, one call's
+//     tail overlaps the next call's head, and FP64 (DMMA) and FP32 (FFMA2)
+//     kernels can co-reside on an SM (different pipes).
+// Ordering is preserved wherever it matters: a call waits for every earlier
+// call whose device write window overlaps its device reads or writes (or vice
+// versa), and host inputs that an earlier call's copy-out writes are read
+// only after that copy-out.
 #include <algorithm>
 #include <mutex>
 #include <vector>
@@ -29,10 +35,14 @@ bool is_device_ptr(const void* ptr) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+constexpr int kComputeStreams = 4;
+constexpr size_t kDepth = 3;  // host-staged calls allowed in flight (bounds staging memory)
+
 // Per-device copy-in / compute / copy-out streams (blocking streams, so they
 // stay ordered with the legacy default stream other libraries use).
 struct Streams {
-  cudaStream_t in = nullptr, compute = nullptr, out = nullptr;
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaStream_t compute[kComputeStreams] = {};
 };
 
 Streams device_streams() {
@@ -43,10 +53,10 @@ Streams device_streams() {
   std::lock_guard<std::mutex> lock(mu);
   if (cache.size() <= static_cast<size_t>(dev)) cache.resize(dev + 1);
   Streams& s = cache[dev];
-  if (!s.compute) {
+  if (!s.in) {
     cuda_check(cudaStreamCreate(&s.in), "stream");
-    cuda_check(cudaStreamCreate(&s.compute), "stream");
     cuda_check(cudaStreamCreate(&s.out), "stream");
+    for (cudaStream_t& c : s.compute) cuda_check(cudaStreamCreate(&c), "stream");
   }
   return s;
 }
@@ -54,16 +64,181 @@ Streams device_streams() {
 struct Window {
   const std::byte* lo = nullptr;
   const std::byte* hi = nullptr;
-  bool overlaps(const Window& o) const { return lo < o.hi && o.lo < hi; }
+  bool empty() const { return hi <= lo; }
+  bool overlaps(const Window& o) const { return !empty() && !o.empty() && lo < o.hi && o.lo < hi; }
 };
 
-struct Inflight {
+struct Call {
+  ExecutionPlan plan;
+  Window win[3];       // A, B, C byte windows as the caller gave them
+  bool host[3] = {};   // operand lives in host memory (staged)
+  bool active = false; // m, n > 0
+  // device footprint (unstaged operands only)
+  Window dev_read[3];
+  Window dev_write;
+  Window host_write;   // host window written by the copy-out
   std::vector<void*> buffers;
   cudaEvent_t in_done = nullptr, comp_done = nullptr, out_done = nullptr;
-  Window c_host;  // host window written by this call's copy-out (empty if none)
+  int stream = 0;
 };
 
-constexpr size_t kDepth = 3;  // calls allowed in flight (bounds staging memory)
+cudaEvent_t new_event() {
+  cudaEvent_t e = nullptr;
+  cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  return e;
+}
+
+void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc) {
+  // Every plan first: policy and shape errors surface before any device work.
+  std::vector<Call> cs(calls.size());
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const GemmCall& g = calls[i];
+    if (ranges_overlap(g.c, g.a) || ranges_overlap(g.c, g.b)) throw Error("gemm: C must not alias A or B");
+    cs[i].plan = plan(g.alpha, g.a, g.b, g.beta, g.c, cfg);
+  }
+  const Streams S = device_streams();
+  // fork from the caller's stream
+  cudaEvent_t fork = new_event();
+  cuda_check(cudaEventRecord(fork, user), "event");
+  cuda_check(cudaStreamWaitEvent(S.in, fork, 0), "fork");
+  for (cudaStream_t c : S.compute) cuda_check(cudaStreamWaitEvent(c, fork, 0), "fork");
+  cuda_check(cudaStreamWaitEvent(S.out, fork, 0), "fork");
+
+  auto cleanup = [&](bool wait) {
+    if (wait) {
+      cudaStreamSynchronize(S.in);
+      for (cudaStream_t c : S.compute) cudaStreamSynchronize(c);
+      cudaStreamSynchronize(S.out);
+    }
+    for (Call& c : cs) {
+      for (void* q : c.buffers) cudaFree(q);
+      c.buffers.clear();
+      for (cudaEvent_t e : {c.in_done, c.comp_done, c.out_done})
+        if (e) cudaEventDestroy(e);  // destruction is deferred until the event completes
+    }
+    cudaEventDestroy(fork);
+  };
+  try {
+    size_t staged = 0;  // host-staged calls issued so far (for the in-flight throttle)
+    std::vector<size_t> staged_ids;
+    int rr = 0;
+    for (size_t i = 0; i < calls.size(); ++i) {
+      Call& c = cs[i];
+      ExecutionPlan& p = c.plan;
+      c.active = p.m > 0 && p.n > 0;
+      c.in_done = new_event();
+      c.comp_done = new_event();
+      c.out_done = new_event();
+      const MatrixView* originals[3] = {&calls[i].a, &calls[i].b, &calls[i].c};
+      const bool need[3] = {c.active && p.k > 0, c.active && p.k > 0, c.active};
+      bool any_host = false;
+      for (int r = 0; r < 3; ++r) {
+        const auto [lo, hi] = byte_range(*originals[r]);
+        c.win[r] = Window{lo, hi};
+        if (!need[r] || c.win[r].empty()) continue;
+        c.host[r] = !is_device_ptr(lo);
+        any_host = any_host || c.host[r];
+        if (!c.host[r]) c.dev_read[r] = c.win[r];
+      }
+      if (need[2] && !c.host[2]) c.dev_write = c.win[2];
+
+      // Device-memory conflicts with earlier calls: for every compute stream
+      // the most recent conflicting call (waiting for it covers the earlier
+      // ones on that stream).  The call joins the stream of its latest
+      // conflict -- a dependency chain stays on one stream -- or, without
+      // conflicts, the next stream round-robin.
+      auto conflicts = [&](const Call& e) {
+        if (e.dev_write.overlaps(c.dev_write)) return true;
+        for (int r = 0; r < 3; ++r)
+          if (e.dev_write.overlaps(c.dev_read[r]) || c.dev_write.overlaps(e.dev_read[r])) return true;
+        return false;
+      };
+      long latest[kComputeStreams];
+      std::fill(latest, latest + kComputeStreams, -1L);
+      long newest = -1;
+      int unresolved = kComputeStreams;
+      for (long h = static_cast<long>(i) - 1; h >= 0 && unresolved > 0; --h) {
+        const Call& e = cs[static_cast<size_t>(h)];
+        if (latest[e.stream] >= 0 || !conflicts(e)) continue;
+        latest[e.stream] = h;
+        --unresolved;
+        newest = std::max(newest, h);
+      }
+      if (newest >= 0) {
+        c.stream = cs[static_cast<size_t>(newest)].stream;
+      } else {
+        c.stream = rr;
+        rr = (rr + 1) % kComputeStreams;
+      }
+      cudaStream_t cst = S.compute[c.stream];
+
+      // ---- copy-in of host operands
+      std::byte* dev[3] = {nullptr, nullptr, nullptr};
+      if (any_host) {
+        if (staged >= kDepth)
+          cuda_check(cudaStreamWaitEvent(S.in, cs[staged_ids[staged - kDepth]].out_done, 0), "throttle");
+        staged_ids.push_back(i);
+        ++staged;
+        for (int r = 0; r < 3; ++r) {
+          if (!need[r] || !c.host[r] || c.win[r].empty()) continue;
+          for (size_t h = 0; h < i; ++h)  // host read-after-write through an earlier copy-out
+            if (cs[h].host_write.overlaps(c.win[r])) cuda_check(cudaStreamWaitEvent(S.in, cs[h].out_done, 0), "dep");
+          for (size_t h = 0; h < i; ++h)  // device-resident C of an earlier call copied from the same host bytes
+            if (cs[h].dev_write.overlaps(c.win[r])) cuda_check(cudaStreamWaitEvent(S.in, cs[h].comp_done, 0), "dep");
+          void* d = nullptr;
+          const size_t bytes = static_cast<size_t>(c.win[r].hi - c.win[r].lo);
+          cuda_check(cudaMallocAsync(&d, bytes, S.in), "staging allocation");
+          c.buffers.push_back(d);
+          dev[r] = static_cast<std::byte*>(d);
+          cuda_check(cudaMemcpyAsync(d, c.win[r].lo, bytes, cudaMemcpyHostToDevice, S.in), "H2D staging");
+        }
+        cuda_check(cudaEventRecord(c.in_done, S.in), "event");
+        cuda_check(cudaStreamWaitEvent(cst, c.in_done, 0), "dependency");
+      }
+      auto rebase = [&](MatrixView& v) {
+        for (int r = 0; r < 3; ++r)
+          if (dev[r] && v.base >= c.win[r].lo && v.base < c.win[r].hi) {
+            v.base = dev[r] + (v.base - c.win[r].lo);
+            return;
+          }
+      };
+      rebase(p.a);
+      rebase(p.b);
+      rebase(p.c);
+
+      // ---- device-memory dependencies on earlier calls on other streams
+      for (int s = 0; s < kComputeStreams; ++s)
+        if (s != c.stream && latest[s] >= 0)
+          cuda_check(cudaStreamWaitEvent(cst, cs[static_cast<size_t>(latest[s])].comp_done, 0), "dependency");
+
+      execute(p, cfg.numerics, cst, fc);
+      cuda_check(cudaEventRecord(c.comp_done, cst), "event");
+
+      // ---- copy-out of a host C, release of staging
+      if (any_host) {
+        cuda_check(cudaStreamWaitEvent(S.out, c.comp_done, 0), "dependency");
+        if (dev[2]) {
+          c.host_write = c.win[2];
+          cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(c.win[2].lo), dev[2],
+                                     static_cast<size_t>(c.win[2].hi - c.win[2].lo), cudaMemcpyDeviceToHost, S.out),
+                     "D2H staging");
+        }
+        for (void* q : c.buffers) cuda_check(cudaFreeAsync(q, S.out), "staging release");
+        c.buffers.clear();
+        cuda_check(cudaEventRecord(c.out_done, S.out), "event");
+      } else {
+        cuda_check(cudaEventRecord(c.out_done, cst), "event");
+      }
+    }
+    // join back into the caller's stream
+    for (const Call& c : cs) cuda_check(cudaStreamWaitEvent(user, c.out_done, 0), "join");
+    if (sync) cuda_check(cudaStreamSynchronize(user), "gemm synchronisation");
+  } catch (...) {
+    cleanup(true);
+    throw;
+  }
+  cleanup(false);
+}
 
 }  // namespace
 
@@ -75,90 +250,11 @@ void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar b
 }
 
 void gemm_batch(const std::vector<GemmCall>& calls, const Config& cfg, FlopCounter* fc) {
-  // Every plan first: policy and shape errors surface before any device work.
-  std::vector<ExecutionPlan> plans;
-  plans.reserve(calls.size());
-  for (const GemmCall& g : calls) {
-    if (ranges_overlap(g.c, g.a) || ranges_overlap(g.c, g.b)) throw Error("gemm: C must not alias A or B");
-    plans.push_back(plan(g.alpha, g.a, g.b, g.beta, g.c, cfg));
-  }
-  const Streams S = device_streams();
-  std::vector<Inflight> fl(calls.size());
-  auto event = [] {
-    cudaEvent_t e = nullptr;
-    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    return e;
-  };
-  auto cleanup = [&] {
-    cudaStreamSynchronize(S.in);
-    cudaStreamSynchronize(S.compute);
-    cudaStreamSynchronize(S.out);
-    for (Inflight& f : fl) {
-      for (void* q : f.buffers) cudaFree(q);  // normally already released stream-ordered
-      f.buffers.clear();
-      for (cudaEvent_t e : {f.in_done, f.comp_done, f.out_done})
-        if (e) cudaEventDestroy(e);
-    }
-  };
-  try {
-    for (size_t i = 0; i < calls.size(); ++i) {
-      ExecutionPlan p = plans[i];
-      Inflight& f = fl[i];
-      f.in_done = event();
-      f.comp_done = event();
-      f.out_done = event();
-      if (i >= kDepth) cuda_check(cudaStreamWaitEvent(S.in, fl[i - kDepth].out_done, 0), "throttle");
-      const MatrixView* originals[3] = {&calls[i].a, &calls[i].b, &calls[i].c};
-      const bool needed = p.m > 0 && p.n > 0;
-      const bool need[3] = {needed && p.k > 0, needed && p.k > 0, needed};
-      Window win[3];
-      std::byte* dev[3] = {nullptr, nullptr, nullptr};
-      for (int r = 0; r < 3; ++r) {
-        const auto [lo, hi] = byte_range(*originals[r]);
-        win[r] = Window{lo, hi};
-        if (!need[r] || hi <= lo || is_device_ptr(lo)) continue;
-        // read-after-write on host memory written by an earlier copy-out
-        for (size_t h = 0; h < i; ++h)
-          if (fl[h].c_host.overlaps(win[r])) cuda_check(cudaStreamWaitEvent(S.in, fl[h].out_done, 0), "dependency");
-        void* d = nullptr;
-        const size_t bytes = static_cast<size_t>(hi - lo);
-        cuda_check(cudaMallocAsync(&d, bytes, S.in), "staging allocation");
-        f.buffers.push_back(d);
-        dev[r] = static_cast<std::byte*>(d);
-        cuda_check(cudaMemcpyAsync(d, lo, bytes, cudaMemcpyHostToDevice, S.in), "H2D staging");
-      }
-      auto rebase = [&](MatrixView& v) {
-        for (int r = 0; r < 3; ++r)
-          if (dev[r] && v.base >= win[r].lo && v.base < win[r].hi) {
-            v.base = dev[r] + (v.base - win[r].lo);
-            return;
-          }
-      };
-      rebase(p.a);
-      rebase(p.b);
-      rebase(p.c);
-      cuda_check(cudaEventRecord(f.in_done, S.in), "event");
-      cuda_check(cudaStreamWaitEvent(S.compute, f.in_done, 0), "dependency");
-      execute(p, cfg.numerics, S.compute, fc);
-      cuda_check(cudaEventRecord(f.comp_done, S.compute), "event");
-      cuda_check(cudaStreamWaitEvent(S.out, f.comp_done, 0), "dependency");
-      if (dev[2]) {
-        f.c_host = win[2];
-        cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(win[2].lo), dev[2], static_cast<size_t>(win[2].hi - win[2].lo),
-                                   cudaMemcpyDeviceToHost, S.out),
-                   "D2H staging");
-      }
-      for (void* q : f.buffers) cuda_check(cudaFreeAsync(q, S.out), "staging release");
-      f.buffers.clear();
-      cuda_check(cudaEventRecord(f.out_done, S.out), "event");
-    }
-    cuda_check(cudaStreamSynchronize(S.out), "gemm synchronisation");
-    cuda_check(cudaStreamSynchronize(S.compute), "gemm synchronisation");
-  } catch (...) {
-    cleanup();
-    throw;
-  }
-  cleanup();
+  run_batch(calls, cfg, cudaStreamLegacy, true, fc);
+}
+
+void gemm_batch_async(const std::vector<GemmCall>& calls, const Config& cfg, void* stream, FlopCounter* fc) {
+  run_batch(calls, cfg, stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy, false, fc);
 }
 
 void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,

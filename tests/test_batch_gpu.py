@@ -38,6 +38,33 @@ def test_batch_equals_sequential_calls(numerics):
         assert shared_c[dt].buf.tobytes() == ref_c[dt].buf.tobytes(), dt
 
 
+@pytest.mark.parametrize("numerics", ["exact", "fast"])
+def test_device_batch_concurrency_keeps_order(numerics):
+    """Device-resident calls: independent ones may run concurrently, but RAW
+    (C feeds a later A), WAR (a later call overwrites an earlier call's B) and
+    WAW (shared C) must keep the sequential result."""
+    import torch
+    cfg = config({"gpu.numerics": numerics})
+    n = 96
+    mats = {name: HostMatrix(M.DT_D, n, n).fill(O.orc_rng_state(3, [name])) for name in "PQRSTUVW"}
+    seq = [("P", "Q", "R"), ("S", "T", "U"), ("R", "Q", "V"),  # RAW: R written by 0, read by 2
+           ("P", "T", "Q"),                                   # WAR: Q read by 0 and 2, written here
+           ("S", "P", "R"), ("U", "V", "W"), ("P", "Q", "W"), ("W", "S", "T")]
+    # sequential reference with the oracle (EXACT) or one gemm per call (FAST)
+    ref = {k: v.clone() for k, v in mats.items()}
+    for a, b, c in seq:
+        if numerics == "exact":
+            O.orc_gemm(SCALARS["p7"], ref[a].view(), ref[b].view(), SCALARS["m3"], ref[c].view(), cfg)
+        else:
+            M.gemm(SCALARS["p7"], ref[a].view(), ref[b].view(), SCALARS["m3"], ref[c].view(), cfg)
+    dev = {k: v.to_device() for k, v in mats.items()}
+    M.gemm_batch([(SCALARS["p7"], dev[a].view(), dev[b].view(), SCALARS["m3"], dev[c].view()) for a, b, c in seq],
+                 cfg)
+    torch.cuda.synchronize()
+    for k in mats:
+        assert dev[k].bytes().tobytes() == ref[k].buf.tobytes(), k
+
+
 def test_batch_output_feeds_next_input():
     # call 2 reads call 1's C as its A (host RAW through the copy-out)
     A1 = HostMatrix(M.DT_D, 64, 64).fill(1)
