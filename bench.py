@@ -232,7 +232,6 @@ def run_b200(args):
         dist.barrier()
     sampler = ClockSampler(local)
     launches0 = M.launch_count()
-    M.profile_begin()
     step_ms = []
     for _ in range(args.steps):
         flush.fill_(1)  # L2 flush between timed steps (outside the events)
@@ -243,10 +242,22 @@ def run_b200(args):
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
-    kstats = M.profile_end()
     launches = M.launch_count() - launches0
     clocks = sampler.stop()
     total_ms = sum(step_ms)
+
+    # Per-kernel roofline: inside the timed steps independent calls overlap on
+    # several streams, so a launch's event span is not its own duration; one
+    # extra step runs the same calls serialized on the timed stream, each
+    # kernel bracketed by CUDA events (mdg_profile_begin/end).
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    M.profile_begin()
+    for al, va, vb, be, vc in calls:
+        M.gemm_async(al, va, vb, be, vc, cfg, stream)
+    torch.cuda.synchronize()
+    kstats = M.profile_end()
+    serial_ms = sum(v["ms"] for v in kstats.values())
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -281,7 +292,8 @@ def run_b200(args):
                 "kernel": "gemm_dmma (DMMA.8x8x4 fp64 tensor pipe)" if dom == "dmma" else "gemm_ffma (FFMA fp32)",
                 "peak_source": "measured: tools/peaks.cu on this pool's B200 (profiles/peaks_r01.json)",
                 "algorithmic_work": "2*me*ne*ke real flops per launch (= flops_of_case, the 1m reduction has no waste)"}
-    kernel_share = {k: round(v["ms"] / total_ms, 4) if total_ms else 0 for k, v in kstats.items() if v["launches"]}
+    roof["measured"] = "one serialized step after the timed region, CUDA events around every launch"
+    kernel_share = {k: round(v["ms"] / serial_ms, 4) if serial_ms else 0 for k, v in kstats.items() if v["launches"]}
 
     # ---- e2e: public gemm() on pinned host buffers, H2D + D2H inside the timed region
     e2e = None
@@ -349,6 +361,7 @@ def run_b200(args):
         "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},
         "roofline": roof,
         "kernel_share": kernel_share,
+        "serialized_step_ms": serial_ms,
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
