@@ -1,0 +1,145 @@
+"""Parity at BASELINE.json's full sizes.
+
+The oracle cannot run a 16384^3 problem, so each config is run in full on the
+GPU and checked through properties that do not depend on size:
+  * sampled sub-blocks: rows R x columns S of C (edges included) against the
+    oracle run on A[R, :], B[:, S], C[R, S] with the FULL inner dimension --
+    for the reference this sub-problem is bitwise the same computation as the
+    full one, so EXACT must match bitwise and FAST must meet the
+    reference's per-element bound;
+  * determinism: the same call twice gives the same bits;
+  * exact scaling: alpha = 2 doubles every product exactly, so with beta = 0
+    C(alpha=2) == 2 * C(alpha=1) bitwise.
+Inputs are drawn on the device with the reference's Rng (mdg_fill_uniform)."""
+import numpy as np
+import pytest
+
+import paper_1901_06015_b200 as M
+from oracle import oracle as O
+from tests.helpers import HostMatrix, config
+
+pytestmark = pytest.mark.gpu
+
+TORCH_T = {M.DT_S: "float32", M.DT_D: "float64", M.DT_C: "complex64", M.DT_Z: "complex128"}
+
+
+class DevMat:
+    """Column-major device matrix filled from the reference Rng."""
+
+    def __init__(self, dtype, m, n, state=None):
+        import torch
+        self.dtype, self.m, self.n = dtype, m, n
+        self.t = torch.zeros(m * n * M.dtype_size(dtype), dtype=torch.uint8, device="cuda")
+        if state is not None:
+            M.fill_uniform(self.view(), state)
+
+    def view(self, comp=None):
+        v = M.MatrixView.make(self.t.data_ptr(), self.m, self.n, 1, self.m, self.dtype)
+        if comp is not None:
+            v.comp_prec = comp
+        return v
+
+    def elements(self):
+        import torch
+        return self.t.view(getattr(torch, TORCH_T[self.dtype])).view(self.n, self.m)  # [j, i]
+
+    def block(self, rows, cols) -> HostMatrix:
+        import torch
+        e = self.elements()
+        r = torch.as_tensor(rows, device="cuda")
+        c = torch.as_tensor(cols, device="cuda")
+        sub = e.index_select(0, c).index_select(1, r).T.contiguous().cpu().numpy()  # |rows| x |cols|
+        h = HostMatrix(self.dtype, len(rows), len(cols))
+        h.values()[:, :] = sub
+        return h
+
+    def copy(self):
+        d = DevMat(self.dtype, self.m, self.n)
+        d.t.copy_(self.t)
+        return d
+
+
+def sample(n, count, rng):
+    picks = {0, n - 1} | set(int(x) for x in rng.integers(0, n, count))
+    return sorted(picks)
+
+
+def run_config(label, m, n, k, alpha, beta, numerics, seed=0, nsamp=12, exact_bitwise=False):
+    import torch
+    dc, da, db = (M.dtype_from_letter(ch) for ch in label[:3])
+    comp = M.SINGLE if label[3] == "s" else M.DOUBLE
+    root = M.Rng(seed).split(label).split("scale")
+    A = DevMat(da, m, k, root.split("a").state)
+    B = DevMat(db, k, n, root.split("b").state)
+    C = DevMat(dc, m, n, root.split("c").state)
+    rng = np.random.default_rng(seed)
+    rows, cols = sample(m, nsamp, rng), sample(n, nsamp, rng)
+    c_before = C.block(rows, cols)
+    flops = M.gemm(alpha, A.view(), B.view(), beta, C.view(comp), config({"gpu.numerics": numerics}))
+    torch.cuda.synchronize()
+    assert flops > 0
+    a_rows = A.block(rows, list(range(k)))
+    b_cols = B.block(list(range(k)), cols)
+    c_after = C.block(rows, cols)
+    if exact_bitwise:
+        want = c_before.clone()
+        O.orc_gemm(alpha, a_rows.view(), b_cols.view(), beta, want.view(comp=comp))
+        assert c_after.buf.tobytes() == want.buf.tobytes(), label
+    viol = O.orc_violation(alpha, a_rows.view(), b_cols.view(), beta, c_before.view(comp=comp),
+                           c_after.view(comp=comp), comp)
+    assert viol <= 1.0, (label, viol)
+    return A, B, C
+
+
+def test_cfg1_dssd_1024_full_exact_and_fast():
+    # configs[0]: small enough for the oracle on the whole matrix
+    one = M.Scalar.real_value(1.0)
+    run_config("dssd", 1024, 1024, 1024, one, one, "exact", nsamp=40, exact_bitwise=True)
+    run_config("dssd", 1024, 1024, 1024, one, one, "fast", nsamp=40)
+
+
+def test_cfg3_zzzd_8192():
+    alpha, one = M.Scalar.complex_value(0.5, 1.5), M.Scalar.real_value(1.0)
+    run_config("zzzd", 8192, 8192, 8192, alpha, one, "fast")
+    run_config("zzzd", 8192, 8192, 8192, alpha, one, "exact", exact_bitwise=True, nsamp=6)
+
+
+@pytest.mark.parametrize("label", ["cdds", "szzs", "zczd"])
+def test_cfg4_16384(label):
+    zero, one = M.Scalar.real_value(0.0), M.Scalar.real_value(1.0)
+    run_config(label, 16384, 16384, 16384, one, zero, "fast", nsamp=6)
+
+
+@pytest.mark.parametrize("k", [64, 256, 1024])
+def test_cfg5_rank_k_32768(k):
+    run_config("sddd", 32768, 32768, k, M.Scalar.real_value(-1.0), M.Scalar.real_value(1.0), "fast", nsamp=16)
+
+
+def test_cfg2_sweep_corner_4096():
+    # the sweep's largest size on a label of every case, with the sweep's scalars
+    for label in ("dddd", "zdds", "ddzd", "zdds", "zzzs", "czss", "zdzd", "zzzd"):
+        cid = M.CaseLabel.parse(label).case_id()
+        alpha = M.Scalar.complex_value(1.2, -0.7) if cid in (0, 7) else M.Scalar.real_value(1.2)
+        run_config(label, 4096, 4096, 4096, alpha, M.Scalar.complex_value(0.9, 0.3), "fast", nsamp=6)
+
+
+@pytest.mark.parametrize("label", ["zzzd", "cdds", "sddd", "szzs"])
+def test_determinism_and_exact_power_of_two_scaling(label):
+    import torch
+    m = n = k = 2048
+    zero = M.Scalar.real_value(0.0)
+    one, two = M.Scalar.real_value(1.0), M.Scalar.real_value(2.0)
+    dc, da, db = (M.dtype_from_letter(ch) for ch in label[:3])
+    comp = M.SINGLE if label[3] == "s" else M.DOUBLE
+    root = M.Rng(3).split(label)
+    A = DevMat(da, m, k, root.split("a").state)
+    B = DevMat(db, k, n, root.split("b").state)
+    C1, C2, C3 = DevMat(dc, m, n), DevMat(dc, m, n), DevMat(dc, m, n)
+    cfg = config({"gpu.numerics": "fast"})
+    M.gemm(one, A.view(), B.view(), zero, C1.view(comp), cfg)
+    M.gemm(one, A.view(), B.view(), zero, C2.view(comp), cfg)
+    M.gemm(two, A.view(), B.view(), zero, C3.view(comp), cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(C1.t, C2.t)  # bitwise deterministic
+    e1, e3 = C1.elements(), C3.elements()
+    assert torch.equal(e1 * 2, e3)  # alpha = 2 scales every partial sum exactly
