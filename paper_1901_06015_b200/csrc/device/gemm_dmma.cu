@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
 #pragma unroll
         for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    // generic-proxy reads of the stage before its async-proxy (TMA) refill
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

@@ -114,6 +114,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
         for (int p = 0; p < 4; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][p]) : "l"(ai), "l"(bp[p]));
       }
     }
+    // The stage was read through the generic proxy (LDS); the producer's next
+    // TMA write into it goes through the async proxy.  Order the two before
+    // releasing the slot (without this fence the refill can land before the
+    // reads complete: a cross-proxy WAR race).
+    fence_proxy_async();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
