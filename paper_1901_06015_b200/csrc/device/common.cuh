@@ -161,6 +161,42 @@ struct OutType {
   static constexpr int ESZ = NC * static_cast<int>(sizeof(R));
 };
 
+// accumulate_element on values already in C's storage precision R (t rounded
+// to R, c as stored).  Where the result provably equals the double-precision
+// formulation it is computed in R: for binary32, the exact sum or product of
+// two floats fits in a binary64, so rounding it once to float is the same as
+// rounding it to double and then to float.  That covers beta = 0, beta = 1
+// and a real beta on real C.  A general beta on complex C keeps the
+// complex<double> product of the reference (combine_value).
+template <int CDT>
+__device__ __forceinline__ void combine_typed(const DBeta& beta, bool conj, typename OutType<CDT>::R* c,
+                                              const typename OutType<CDT>::R* t) {
+  using R = typename OutType<CDT>::R;
+  constexpr bool cplx = OutType<CDT>::kComplex;
+  auto add = [](R x, R y) -> R {
+    if constexpr (sizeof(R) == 4) return __fadd_rn(x, y);
+    else return __dadd_rn(x, y);
+  };
+  auto mul = [](R x, R y) -> R {
+    if constexpr (sizeof(R) == 4) return __fmul_rn(x, y);
+    else return __dmul_rn(x, y);
+  };
+  if (beta.is_zero) {
+    c[0] = t[0];
+    if constexpr (cplx) c[1] = t[1];
+  } else if (beta.is_one) {
+    c[0] = add(c[0], t[0]);
+    if constexpr (cplx) c[1] = add(conj ? -c[1] : c[1], t[1]);
+  } else if constexpr (!cplx) {
+    c[0] = add(mul(static_cast<R>(beta.re), c[0]), t[0]);
+  } else {
+    const double2 v = combine_value(CDT, beta, make_double2(c[0], conj ? -static_cast<double>(c[1]) : c[1]),
+                                    t[0], t[1]);
+    c[0] = static_cast<R>(v.x);
+    c[1] = static_cast<R>(v.y);
+  }
+}
+
 // ------------------------------------------------------------ async copies
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -229,17 +265,18 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 // to a component of complex element (r/2, c) / (r, c/2) when the plan pairs
 // rows / columns (virtual_ukr_temp's pairing, kernels.cpp:122-131).
 //
-// The tile is processed in column chunks.  For each chunk the threads stage
-// their accumulators in shared memory, already rounded to C's storage
-// precision and laid out like C (the first step of accumulate_element
-// rounds t to storage precision anyway, so this is exact).  When the C
-// chunk is column-contiguous (rs == 1, full tile, 16-byte aligned columns)
-// it is moved with TMA bulk copies -- one per column, all in flight at once
-// -- and combined in place by a rolled loop; otherwise the loop reads and
-// writes C directly.  `emit(put)` must call put(r, c, value) for every
-// accumulator the calling thread holds.  Code size matters here: this runs
-// once per tile after a long mainloop, so it is a compact rolled loop over a
-// chunk rather than an unrolled per-register sequence.
+// The tile is processed in column chunks.  The threads first stage all their
+// accumulators in shared memory, already rounded to C's storage precision and
+// laid out like C (accumulate_element rounds t to storage precision first,
+// so this is exact).  When C is column-contiguous (rs == 1, full tile,
+// 16-byte aligned columns) each chunk of C arrives by TMA bulk copies -- one
+// per column segment, all in flight at once, issued before the staging so
+// they overlap it -- and a rolled loop combines 16-byte vectors in C's own
+// precision (combine_typed) and writes them straight to global memory.
+// Otherwise a rolled scalar loop reads and writes C through its strides.
+// `emit(put)` must call put(r, c, value) for every accumulator the calling
+// thread holds.  Code size matters: this runs once per tile after a long
+// mainloop, so it stays a compact rolled loop.
 template <int CDT, class Emit>
 __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t region, uint64_t* cbar,
                                               const DEpilogue& e, int64_t r0, int64_t c0, int BM, int BN, int tid,
@@ -247,83 +284,80 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
   using O = OutType<CDT>;
   using R = typename O::R;
   constexpr int NC = O::NC;
+  constexpr int VEC = 16 / O::ESZ;  // output elements per 16-byte vector
   const bool prow = e.pair == MDG_PAIR_ROWS, pcol = e.pair == MDG_PAIR_COLS;
   const int orows = prow ? BM / 2 : BM, ocols = pcol ? BN / 2 : BN;
   const int64_t oi0 = prow ? r0 / 2 : r0, oj0 = pcol ? c0 / 2 : c0;
   const int64_t om = prow ? e.me / 2 : e.me, on = pcol ? e.ne / 2 : e.ne;  // output extent
   const bool reads_c = !e.beta.is_zero;
+  const bool conj = e.out.conj != 0;
   const uint32_t col_bytes = orows * O::ESZ;
   R* const out = reinterpret_cast<R*>(e.out.base);
   const uint64_t first = reinterpret_cast<uint64_t>(out + (oi0 * e.out.rs + oj0 * e.out.cs) * NC);
   const bool tma = e.out.rs == 1 && oi0 + orows <= om && oj0 + ocols <= on && (first & 15) == 0 &&
                    (col_bytes & 15) == 0 && ((e.out.cs * O::ESZ) & 15) == 0;
-  // The whole accumulator tile is staged first (so no accumulator stays live
-  // past this point); C then streams through the rest of the region.
   unsigned char* tbuf = smem;
   unsigned char* cbuf = smem + ocols * col_bytes;
   const int CH = tma ? min(ocols, static_cast<int>((region - ocols * col_bytes) / col_bytes)) : ocols;
-  if (tma && reads_c && tid == 0) fence_proxy_async();
+  auto load_chunk = [&](int j0) {
+    const int ch = min(CH, ocols - j0);
+    fence_proxy_async();
+    mbar_arrive_expect_tx(cbar, ch * col_bytes);
+    for (int j = 0; j < ch; ++j)
+      bulk_g2s(cbuf + j * col_bytes, out + (oi0 + (oj0 + j0 + j) * e.out.cs) * NC, col_bytes, cbar);
+  };
+  if (tma && reads_c && tid == 0) load_chunk(0);
   emit([&](int r, int c, double v) {
     const int oi = prow ? r >> 1 : r, oj = pcol ? c >> 1 : c;
     const int comp = prow ? (r & 1) : (pcol ? (c & 1) : 0);
     reinterpret_cast<R*>(tbuf)[(oj * orows + oi) * NC + comp] = static_cast<R>(v);
   });
+  named_sync(1, nthr);
   uint32_t phase = 0;
 
   for (int j0 = 0; j0 < ocols; j0 += CH) {
     const int ch = min(CH, ocols - j0);
-    if (tma && reads_c && tid == 0) {
-      mbar_arrive_expect_tx(cbar, ch * col_bytes);
-      for (int j = 0; j < ch; ++j)
-        bulk_g2s(cbuf + j * col_bytes, out + (oi0 + (oj0 + j0 + j) * e.out.cs) * NC, col_bytes, cbar);
-    }
-    named_sync(1, nthr);
-    const int n = ch * orows;
     if (tma) {
       if (reads_c) {
         mbar_wait(cbar, phase);
         phase ^= 1;
       }
-      for (int idx = tid; idx < n; idx += nthr) {
-        R* cp = reinterpret_cast<R*>(cbuf) + idx * NC;
-        const R* tp = reinterpret_cast<const R*>(tbuf) + (j0 * orows + idx) * NC;
-        double2 c = make_double2(0.0, 0.0);
-        if (reads_c) {
-          c.x = cp[0];
-          if (NC == 2) c.y = e.out.conj ? -static_cast<double>(cp[1]) : static_cast<double>(cp[1]);
-        }
-        const double2 v = combine_value(CDT, e.beta, c, tp[0], NC == 2 ? static_cast<double>(tp[NC - 1]) : 0.0);
-        cp[0] = static_cast<R>(v.x);
-        if (NC == 2) cp[NC - 1] = static_cast<R>(v.y);
+      const int nv = ch * orows / VEC;
+      for (int v = tid; v < nv; v += nthr) {
+        const int idx = v * VEC;  // element within the chunk, column-major
+        const int oi = idx % orows, oj = idx / orows;
+        union {
+          uint4 u;
+          R x[VEC * NC];
+        } cv, tv;
+        tv.u = *reinterpret_cast<const uint4*>(tbuf + (static_cast<size_t>(j0) * orows + idx) * O::ESZ);
+        cv.u = reads_c ? *reinterpret_cast<const uint4*>(cbuf + static_cast<size_t>(idx) * O::ESZ) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) combine_typed<CDT>(e.beta, conj, &cv.x[u * NC], &tv.x[u * NC]);
+        *reinterpret_cast<uint4*>(out + (oi0 + oi + (oj0 + j0 + oj) * e.out.cs) * NC) = cv.u;
       }
-      fence_proxy_async();
-      named_sync(1, nthr);
-      if (tid == 0) {
-        for (int j = 0; j < ch; ++j)
-          bulk_s2g(out + (oi0 + (oj0 + j0 + j) * e.out.cs) * NC, cbuf + j * col_bytes, col_bytes);
-        bulk_commit();
-        bulk_wait_read();
+      if (j0 + ch < ocols) {  // another chunk will land in cbuf: order these reads before it
+        fence_proxy_async();
+        named_sync(1, nthr);
+        if (reads_c && tid == 0) load_chunk(j0 + ch);
       }
     } else {
+      const int n = ch * orows;
       for (int idx = tid; idx < n; idx += nthr) {
         const int oi = idx % orows, oj = idx / orows;
         const int64_t gi = oi0 + oi, gj = oj0 + j0 + oj;
         if (gi >= om || gj >= on) continue;
         R* cp = out + (gi * e.out.rs + gj * e.out.cs) * NC;
-        const R* tp = reinterpret_cast<const R*>(tbuf) + (j0 * orows + idx) * NC;
-        double2 c = make_double2(0.0, 0.0);
-        if (reads_c) {
-          c.x = cp[0];
-          if (NC == 2) c.y = e.out.conj ? -static_cast<double>(cp[1]) : static_cast<double>(cp[1]);
-        }
-        const double2 v = combine_value(CDT, e.beta, c, tp[0], NC == 2 ? static_cast<double>(tp[NC - 1]) : 0.0);
-        cp[0] = static_cast<R>(v.x);
-        if (NC == 2) cp[NC - 1] = static_cast<R>(v.y);
+        R cv[NC];
+        const R* tp = reinterpret_cast<const R*>(tbuf) + (static_cast<size_t>(j0) * orows + idx) * NC;
+#pragma unroll
+        for (int u = 0; u < NC; ++u) cv[u] = reads_c ? cp[u] : R(0);
+        combine_typed<CDT>(e.beta, conj, cv, tp);
+#pragma unroll
+        for (int u = 0; u < NC; ++u) cp[u] = cv[u];
       }
     }
-    named_sync(1, nthr);  // chunk buffers are free again
   }
-  if (tma && tid == 0) bulk_wait_all();
 }
 
 // Grouped tile raster: walks `group` tile-rows at a time.  A short group
