@@ -187,6 +187,22 @@ std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Da
 void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (p.m == 0 || p.n == 0) return;
+  // Device-ordered entry points need device operands; a host pointer here
+  // would fault inside a kernel and poison the context, so refuse it.
+  auto require_device = [](const MatrixView& v, const char* what) {
+    if (v.m == 0 || v.n == 0) return;
+    cudaPointerAttributes attr{};
+    const cudaError_t e = cudaPointerGetAttributes(&attr, v.base);
+    if (e != cudaSuccess) cudaGetLastError();
+    if (e != cudaSuccess || (attr.type != cudaMemoryTypeDevice && attr.type != cudaMemoryTypeManaged))
+      throw Error(std::string("execute: operand ") + what +
+                  " is not in device memory (use gemm()/gemm_batch() for host operands)");
+  };
+  require_device(p.c, "C");
+  if (p.k > 0) {
+    require_device(p.a, "A");
+    require_device(p.b, "B");
+  }
   if (p.k == 0) {
     if (!p.beta.is_one()) {
       prof::Scope scope(MDG_KERNEL_BETA, st, 2.0 * p.c.m * p.c.n * dtype_size(p.c.dtype));

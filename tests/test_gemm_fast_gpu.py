@@ -116,6 +116,20 @@ def test_scalar_policy_rejection_before_device_work():
     assert np.array_equal(before, dC.bytes())
 
 
+def test_stream_ordered_entry_points_refuse_host_operands():
+    p = Problem("dddd", 8, 8, 8)
+    va, vb, vc = p.views()  # host memory
+    with pytest.raises(M.Error, match="device memory"):
+        M.gemm_async(SCALARS["one"], va, vb, SCALARS["one"], vc)
+    pl = M.plan(SCALARS["one"], va, vb, SCALARS["one"], vc)
+    with pytest.raises(M.Error, match="device memory"):
+        M.execute(pl)
+    # the context is still healthy afterwards
+    dA, dB, dC = p.device()
+    da, db, dc = p.views(A=dA, B=dB, C=dC)
+    M.gemm(SCALARS["one"], da, db, SCALARS["one"], dc)
+
+
 def test_alias_rejected():
     h = HostMatrix(M.DT_D, 4, 4).fill(3).to_device()
     with pytest.raises(M.Error):
