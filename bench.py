@@ -170,9 +170,18 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Test hook: MDGEMM_BENCH_BACKEND=gloo runs the multi-rank path functionally
+    # with several ranks on fewer GPUs (host-staged collectives, no rank ever
+    # waits on another rank's kernels).  Production runs use NCCL, one GPU each.
+    backend = os.environ.get("MDGEMM_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
     desc, items, dist_kind = workload(args)
@@ -293,6 +302,18 @@ def run_b200(args):
                 "peak_source": "measured: tools/peaks.cu on this pool's B200 (profiles/peaks_r01.json)",
                 "algorithmic_work": "2*me*ne*ke real flops per launch (= flops_of_case, the 1m reduction has no waste)"}
     roof["measured"] = "one serialized step after the timed region, CUDA events around every launch"
+    kernels = {}
+    for kind, v in kstats.items():
+        if not v["launches"] or not v["ms"]:
+            continue
+        rate = v["work"] / (v["ms"] * 1e-3)
+        if kind in ("pack", "beta", "fill"):
+            kernels[kind] = {"launches": v["launches"], "ms": round(v["ms"], 3), "GB/s": round(rate / 1e9, 1),
+                             "frac_of_hbm": round(rate / 1e9 / pk["hbm_gbs"], 3)}
+        else:
+            peak = pk["dmma_tflops"] if kind == "dmma" else pk["ffma_tflops"]
+            kernels[kind] = {"launches": v["launches"], "ms": round(v["ms"], 3), "TFLOP/s": round(rate / 1e12, 2),
+                             "frac_of_peak": round(rate / 1e12 / peak, 3)}
     kernel_share = {k: round(v["ms"] / serial_ms, 4) if serial_ms else 0 for k, v in kstats.items() if v["launches"]}
 
     # ---- e2e: public gemm() on pinned host buffers, H2D + D2H inside the timed region
@@ -361,6 +382,7 @@ def run_b200(args):
         "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},
         "roofline": roof,
         "kernel_share": kernel_share,
+        "kernels": kernels,
         "serialized_step_ms": serial_ms,
         "gpu_launches": launches,
         "clocks": clocks,
