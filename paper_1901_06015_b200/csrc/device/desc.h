@@ -81,7 +81,10 @@ struct GemmDesc {
   double seed_beta;    // EXACT_DIRECT_SEEDED: beta as passed to gemm_ukr
   DView flat;          // EXACT_ONEM_MIXED: real_flatten(C) of the 1m variant
   int32_t group_rows;  // tile raster group height (0 = default 8)
+  int32_t splits;      // split-K factor of the fast kernels (1 = none)
+  int32_t kb_per_split;  // 16-deep k-blocks per split
   int32_t reserved2;
+  void* partials;      // splits > 1: per (tile, split) accumulator tiles, comp precision
 };
 
 // ---- host launchers (defined in the .cu files) ----
@@ -98,5 +101,10 @@ FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms);
 FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms);
 cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
 cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
+// Split-K: sum the `splits` partial tiles in split order and run the fused
+// epilogue (one CTA per tile).
+cudaError_t launch_splitk_reduce(const GemmDesc& d, const FastTile& t, bool single, cudaStream_t s);
+// Split factor for a problem of `tiles` CTA tiles and `nk` k-blocks (1 = none).
+int choose_splits(int64_t tiles, int64_t nk, int slots);
 
 }  // namespace mdg

@@ -56,12 +56,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
+  const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
+  const int split = static_cast<int>(blockIdx.x / tiles);  // split-K slice of this CTA
+  const int64_t tile_id = blockIdx.x % tiles;
   int tm, tn;
-  tile_coords(blockIdx.x, tiles_m, tiles_n, d.group_rows, tm, tn);
+  tile_coords(tile_id, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
-  const int nk = static_cast<int>(lpad / C::BK);
-  const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
-  const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
+  const int nk_all = static_cast<int>(lpad / C::BK);
+  const int kb0 = d.splits > 1 ? split * d.kb_per_split : 0;
+  const int nk = d.splits > 1 ? min(nk_all - kb0, d.kb_per_split) : nk_all;
+  const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad +
+                     static_cast<int64_t>(kb0) * C::STAGE_A;
+  const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad +
+                     static_cast<int64_t>(kb0) * C::STAGE_B;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -123,6 +130,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
 
   // ------------------------------------------------------------ epilogue
   constexpr int NCT = C::NCW * 32;
+  if (d.splits > 1) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
+    double* part = static_cast<double*>(d.partials) + (split * tiles + tile_id) * (C::BM * C::BN);
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) {
+        const int r = wm * C::WTM + i * 8 + g;
+        const int c = wn * C::WTN + j * 8 + 2 * tig;
+        part[c * C::BM + r] = acc[i][j][0];
+        part[(c + 1) * C::BM + r] = acc[i][j][1];
+      }
+    return;
+  }
   named_sync(1, NCT);  // every consumer is done with the ring
   fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
                      static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, threadIdx.x, NCT, [&](auto&& put) {
@@ -147,7 +167,8 @@ cudaError_t run(const GemmDesc& d, cudaStream_t s) {
     e = cudaFuncSetAttribute(gemm_dmma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
-    gemm_dmma_kernel<C, CDT><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+    gemm_dmma_kernel<C, CDT><<<static_cast<unsigned>(tiles * (d.splits > 1 ? d.splits : 1)), C::THREADS, C::SMEM,
+                               s>>>(d);
   });
   return cudaGetLastError();
 }

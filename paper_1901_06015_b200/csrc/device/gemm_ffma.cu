@@ -48,12 +48,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
+  const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
+  const int split = static_cast<int>(blockIdx.x / tiles);  // split-K slice of this CTA
+  const int64_t tile_id = blockIdx.x % tiles;
   int tm, tn;
-  tile_coords(blockIdx.x, tiles_m, tiles_n, d.group_rows, tm, tn);
+  tile_coords(tile_id, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
-  const int nk = static_cast<int>(lpad / C::BK);
-  const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
-  const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
+  const int nk_all = static_cast<int>(lpad / C::BK);
+  const int kb0 = d.splits > 1 ? split * d.kb_per_split : 0;
+  const int nk = d.splits > 1 ? min(nk_all - kb0, d.kb_per_split) : nk_all;
+  const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad +
+                    static_cast<int64_t>(kb0) * C::STAGE_A;
+  const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad +
+                    static_cast<int64_t>(kb0) * C::STAGE_B;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -124,6 +131,20 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
   }
 
   // ------------------------------------------------------------ epilogue
+  if (d.splits > 1) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
+    float* part = static_cast<float*>(d.partials) + (split * tiles + tile_id) * (C::BM * C::BN);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = __uint_as_float(static_cast<uint32_t>((j & 1) ? (acc[i][j >> 1] >> 32) : acc[i][j >> 1]));
+      *reinterpret_cast<float4*>(&part[c * C::BM + ty * 4]) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(&part[c * C::BM + C::BM / 2 + ty * 4]) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+    return;
+  }
   named_sync(1, C::NCT);  // every consumer is done with the ring
   fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
                      static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, tid, C::NCT, [&](auto&& put) {
@@ -149,7 +170,8 @@ cudaError_t run(const GemmDesc& d, cudaStream_t s) {
     e = cudaFuncSetAttribute(gemm_ffma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
-    gemm_ffma_kernel<C, CDT><<<static_cast<unsigned>(tiles), C::THREADS, C::SMEM, s>>>(d);
+    gemm_ffma_kernel<C, CDT><<<static_cast<unsigned>(tiles * (d.splits > 1 ? d.splits : 1)), C::THREADS, C::SMEM,
+                               s>>>(d);
   });
   return cudaGetLastError();
 }

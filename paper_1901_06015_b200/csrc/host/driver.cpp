@@ -221,9 +221,23 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, tile.bm, lpad);
   Packed pb = prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, tile.bn, lpad);
 
+  // Split-K when the tile grid cannot fill the machine (deterministic: the
+  // partial tiles are summed in split order by the reduce pass).
+  const int64_t tiles = ((p.m + tile.bm - 1) / tile.bm) * ((p.n + tile.bn - 1) / tile.bn);
+  const int per_sm = tile.bm == 64 && tile.bn == 128 ? 2 : (tile.bm == 64 && tile.bn == 64 ? 3 : 1);
+  const int64_t nk = lpad / tile.bk;
+  int splits = exact ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
+  int kb_per_split = static_cast<int>(nk);
+  if (splits > 1) {
+    kb_per_split = static_cast<int>((nk + splits - 1) / splits);
+    splits = static_cast<int>((nk + kb_per_split - 1) / kb_per_split);
+  }
+  const size_t acc_size = single ? sizeof(float) : sizeof(double);
   const size_t off_b = (pa.bytes + 255) / 256 * 256;
+  const size_t off_p = off_b + (pb.bytes + 255) / 256 * 256;
+  const size_t part_bytes = splits > 1 ? static_cast<size_t>(splits * tiles * tile.bm * tile.bn) * acc_size : 0;
   void* ws = nullptr;
-  cuda_check(cudaMallocAsync(&ws, off_b + pb.bytes, st), "workspace allocation");
+  cuda_check(cudaMallocAsync(&ws, off_p + part_bytes, st), "workspace allocation");
   char* wsa = static_cast<char*>(ws);
   cudaError_t err;
   {
@@ -253,6 +267,9 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   // otherwise 8-row groups for A/B panel reuse in L2.
   g.group_rows = p.k <= 512 ? static_cast<int32_t>((p.m + tile.bm - 1) / tile.bm) : 8;
   if (const char* force = std::getenv("MDGEMM_GROUP_ROWS")) g.group_rows = std::atoi(force);
+  g.splits = splits;
+  g.kb_per_split = kb_per_split;
+  g.partials = splits > 1 ? wsa + off_p : nullptr;
 
   if (err == cudaSuccess) {
     if (exact) {
@@ -276,8 +293,15 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
       prof::Scope scope(MDG_KERNEL_EXACT, st, 2.0 * p.m * p.n * p.k);
       err = mdg::launch_gemm_exact(g, single, st);
     } else {
-      prof::Scope scope(single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA, st, 2.0 * p.m * p.n * p.k);
-      err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+      const int kind = single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA;
+      {
+        prof::Scope scope(kind, st, 2.0 * p.m * p.n * p.k);
+        err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+      }
+      if (err == cudaSuccess && splits > 1) {
+        prof::Scope scope(kind, st, 0.0);  // same job: its time counts against the gemm's flops
+        err = mdg::launch_splitk_reduce(g, tile, single, st);
+      }
     }
   }
   const cudaError_t ferr = cudaFreeAsync(ws, st);
