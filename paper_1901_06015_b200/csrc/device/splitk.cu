@@ -47,9 +47,13 @@ int choose_splits(int64_t tiles, int64_t nk, int slots) {
     const int f = std::atoi(force);
     if (f > 0) return static_cast<int>(std::min<int64_t>(f, nk));
   }
-  if (tiles >= slots || nk < 8) return 1;
+  // Measured on B200: 5-6x for small outputs with a long k (256x256x16384),
+  // but a loss on small cubes (512^3, 1024^3) where the extra pass and the
+  // partial traffic cost more than the idle SMs.  Split only when the grid is
+  // at least 2x underfilled and every slice keeps >= 32 k-blocks (512 steps).
+  if (tiles * 2 > slots || nk < 64) return 1;
   int64_t s = (slots + tiles - 1) / tiles;  // enough CTAs for one full wave
-  s = std::min<int64_t>(s, nk / 4);         // at least 4 k-blocks (64 inner steps) per split
+  s = std::min<int64_t>(s, nk / 32);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(s, 16)));
 }
 
