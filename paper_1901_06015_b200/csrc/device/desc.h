@@ -83,8 +83,8 @@ struct GemmDesc {
   int32_t group_rows;  // tile raster group height (0 = default 8)
   int32_t splits;      // split-K factor of the fast kernels (1 = none)
   int32_t kb_per_split;  // 16-deep k-blocks per split
-  int32_t reserved2;
-  void* partials;      // splits > 1: per (tile, split) accumulator tiles, comp precision
+  int32_t prefetch;    // fast kernels: L2 prefetch distance in k-blocks ahead of the ring (0 = off)
+  void* partials;     // splits > 1: per (tile, split) accumulator tiles, comp precision
 };
 
 // ---- host launchers (defined in the .cu files) ----

@@ -85,6 +85,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
     if (lane == 0) {
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
+        if (d.prefetch > 0 && kb + d.prefetch < nk) {
+          const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
+          bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(double));
+          bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(double));
+        }
         if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(double));
         bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A,
@@ -105,18 +110,23 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
 #pragma unroll
     for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // (Register-double-buffered fragments do not fit: 10 warps per SM leave
+  // 168 registers per thread and the 64x32 warp tile's accumulators take 128.)
+  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+  const double* a_base = sA + wm * C::WTM + g + tig * C::BM;
+  const double* b_base = sB + wn * C::WTN + g + tig * C::BN;
   for (int kb = 0; kb < nk; ++kb) {
     const int s = kb % C::STAGES;
-    mbar_wait(&full[s], (kb / C::STAGES) & 1);
-    const double* a = sA + s * C::STAGE_A + wm * C::WTM + g;
-    const double* b = sB + s * C::STAGE_B + wn * C::WTN + g;
+    mbar_wait_u32(full_u + 8 * s, (kb / C::STAGES) & 1);
+    const double* a = a_base + s * C::STAGE_A;
+    const double* b = b_base + s * C::STAGE_B;
 #pragma unroll
     for (int kk = 0; kk < C::BK; kk += 4) {
       double af[C::MT], bf[C::NT];
 #pragma unroll
-      for (int i = 0; i < C::MT; ++i) af[i] = a[(kk + tig) * C::BM + i * 8];
+      for (int i = 0; i < C::MT; ++i) af[i] = a[kk * C::BM + i * 8];
 #pragma unroll
-      for (int j = 0; j < C::NT; ++j) bf[j] = b[(kk + tig) * C::BN + j * 8];
+      for (int j = 0; j < C::NT; ++j) bf[j] = b[kk * C::BN + j * 8];
 #pragma unroll
       for (int i = 0; i < C::MT; ++i)
 #pragma unroll
@@ -125,7 +135,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
     // generic-proxy reads of the stage before its async-proxy (TMA) refill
     fence_proxy_async();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
   }
 
   // ------------------------------------------------------------ epilogue

@@ -77,6 +77,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
     if (tid == C::NCT) {
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % C::STAGES;
+        if (d.prefetch > 0 && kb + d.prefetch < nk) {
+          const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
+          bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(float));
+          bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(float));
+        }
         if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(float));
         bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A,
@@ -100,11 +105,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
 #pragma unroll
     for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
 
+  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+  const float* a_base = sA + ty * 4;
+  const float* b_base = sB + tx * 4;
   for (int kb = 0; kb < nk; ++kb) {
     const int s = kb % C::STAGES;
-    mbar_wait(&full[s], (kb / C::STAGES) & 1);
-    const float* a = sA + s * C::STAGE_A + ty * 4;
-    const float* b = sB + s * C::STAGE_B + tx * 4;
+    mbar_wait_u32(full_u + 8 * s, (kb / C::STAGES) & 1);
+    const float* a = a_base + s * C::STAGE_A;
+    const float* b = b_base + s * C::STAGE_B;
 #pragma unroll
     for (int kk = 0; kk < C::BK; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(a + kk * C::BM);
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
     // reads complete: a cross-proxy WAR race).
     fence_proxy_async();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
   }
 
   // ------------------------------------------------------------ epilogue
@@ -176,9 +184,9 @@ cudaError_t run(const GemmDesc& d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-using Big = FfmaCfg<128, 128, 4, 1>;
-using Pair = FfmaCfg<64, 128, 4, 2>;  // two CTAs per SM: epilogues overlap mainloops
-using Small = FfmaCfg<64, 64, 4, 4>;
+using Big = FfmaCfg<128, 128, 8, 1>;
+using Pair = FfmaCfg<64, 128, 8, 2>;  // two CTAs per SM: epilogues overlap mainloops
+using Small = FfmaCfg<64, 64, 6, 4>;
 
 }  // namespace
 

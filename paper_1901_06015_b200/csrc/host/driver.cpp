@@ -270,6 +270,8 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   g.splits = splits;
   g.kb_per_split = kb_per_split;
   g.partials = splits > 1 ? wsa + off_p : nullptr;
+  g.prefetch = 0;
+  if (const char* force = std::getenv("MDGEMM_PREFETCH")) g.prefetch = std::atoi(force);
 
   if (err == cudaSuccess) {
     if (exact) {
