@@ -257,6 +257,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+  return s;
+}
+
+// Tuning trace: one record of TRACE_WORDS per CTA (desc.h).
+__device__ __forceinline__ void trace_stamp(unsigned long long* trace, unsigned long long t_start,
+                                            unsigned long long t_first, unsigned long long t_loop) {
+  unsigned long long* r = trace + static_cast<size_t>(blockIdx.x) * TRACE_WORDS;
+  r[0] = smid();
+  r[1] = t_start;
+  r[2] = t_first;
+  r[3] = t_loop;
+  r[4] = globaltimer();
+}
+
 // Warm L2 with a global range ahead of the TMA ring (no shared memory, no
 // completion): hides DRAM latency that a STAGES-deep ring cannot.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
@@ -303,7 +325,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 template <int CDT, class Emit>
 __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t region, uint64_t* cbar,
                                               const DEpilogue& e, int64_t r0, int64_t c0, int BM, int BN, int tid,
-                                              int nthr, Emit emit) {
+                                              int nthr, uint32_t& phase, Emit emit) {
   using O = OutType<CDT>;
   using R = typename O::R;
   constexpr int NC = O::NC;
@@ -336,7 +358,6 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
     reinterpret_cast<R*>(tbuf)[(oj * orows + oi) * NC + comp] = static_cast<R>(v);
   });
   named_sync(1, nthr);
-  uint32_t phase = 0;
 
   for (int j0 = 0; j0 < ocols; j0 += CH) {
     const int ch = min(CH, ocols - j0);
@@ -397,6 +418,110 @@ __device__ __forceinline__ void tile_coords(int64_t id, int tiles_m, int tiles_n
   const int64_t in = id % per_group;
   tm = first + static_cast<int>(in % gsize);
   tn = static_cast<int>(in / gsize);
+}
+
+// ---- work schedule of one CTA of the fast kernels ------------------------
+//
+// Classic grid: one segment, the whole k range of tile blockIdx % tiles (or
+// split-K slice blockIdx / tiles of it).
+//
+// Stream-K grid (d.sk_grid = G CTAs, all resident): the tiles x nk k-blocks
+// are cut into G equal contiguous ranges, CTA b owning [b U/G, (b+1) U/G).
+// A range ends inside a tile at most once on each side (ranges are >= one
+// tile long), giving up to three kinds of segment:
+//   SEG_START  the first k-blocks of the tile the range ends in: accumulated
+//              from zero and published to partial slot b (run FIRST, so the
+//              next CTA never waits long);
+//   SEG_FULL   whole tiles;
+//   SEG_END    the rest of the tile the range starts in: the accumulators are
+//              SEEDED with CTA b-1's published partial and the k loop simply
+//              continues (run LAST).
+// Continuing the accumulation instead of adding two partial sums keeps every
+// element's rounding sequence identical to the single-CTA k loop, so the
+// result is bitwise the same as the classic grid (and as any column shard).
+enum SegKind : int { SEG_FULL = 0, SEG_START = 1, SEG_END = 2, SEG_SPLIT = 3 };
+
+struct Seg {
+  int tile;
+  int k0, k1;  // k-block range
+  int kind;
+};
+
+// 32-bit fields: the schedule stays live through the mainloop of a
+// register-bound kernel (tiles and k-blocks per launch are < 2^31).
+struct Sched {
+  int tiles, nk, nseg;
+  int start_tile, start_k1;  // SEG_START (start_k1 == 0: none)
+  int full0;                 // first SEG_FULL tile
+  int end_tile, end_k0;      // SEG_END (end_k0 == 0: none)
+};
+
+// SK is a template flag so the classic kernels compile to one straight
+// segment (the stream-K loop costs registers).
+template <bool SK>
+__device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, int nk) {
+  Sched s{};
+  s.tiles = static_cast<int>(tiles);
+  s.nk = nk;
+  if (!SK) {
+    s.nseg = 1;
+    return s;
+  }
+  // Hybrid grid: the first dp = (tiles / G - 1) * G CTAs take one whole tile
+  // each (hardware-scheduled waves, as in the classic grid); the last G CTAs
+  // share the remaining G + tiles % G tiles as equal k-block ranges.
+  const int64_t G = d.sk_grid;
+  const int64_t dp = (tiles / G - 1) * G;
+  if (static_cast<int64_t>(blockIdx.x) < dp) {
+    s.full0 = static_cast<int>(blockIdx.x);
+    s.start_tile = s.full0 + 1;
+    s.nseg = 1;
+    return s;
+  }
+  const int64_t U = (tiles - dp) * nk, b = blockIdx.x - dp;
+  const int64_t u0 = dp * nk + b * U / G, u1 = dp * nk + (b + 1) * U / G;
+  s.start_tile = static_cast<int>(u1 / nk);
+  s.start_k1 = static_cast<int>(u1 % nk);
+  s.end_tile = static_cast<int>(u0 / nk);
+  s.end_k0 = static_cast<int>(u0 % nk);
+  s.full0 = static_cast<int>((u0 + nk - 1) / nk);
+  s.nseg = (s.start_k1 != 0) + (s.start_tile - s.full0) + (s.end_k0 != 0);
+  return s;
+}
+
+// Stream-K CTA index among the last sk_grid CTAs (partial slots and flags).
+__device__ __forceinline__ int sk_index(const GemmDesc& d, int64_t tiles) {
+  return static_cast<int>(blockIdx.x - (tiles / d.sk_grid - 1) * d.sk_grid);
+}
+
+template <bool SK>
+__device__ __forceinline__ Seg sched_seg(const Sched& s, const GemmDesc& d, int idx) {
+  if (!SK) {
+    const int tile = static_cast<int>(blockIdx.x % s.tiles);
+    if (d.splits > 1) {
+      const int k0 = static_cast<int>(blockIdx.x / s.tiles) * d.kb_per_split;
+      return Seg{tile, k0, min(s.nk, k0 + d.kb_per_split), SEG_SPLIT};
+    }
+    return Seg{tile, 0, s.nk, SEG_FULL};
+  }
+  if (s.start_k1 != 0) {
+    if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
+    --idx;
+  }
+  if (idx < s.start_tile - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
+  return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
+}
+
+__device__ __forceinline__ void flag_release(int* f) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(f), "r"(1) : "memory");
+}
+__device__ __forceinline__ void flag_acquire_wait(const int* f) {
+  uint32_t v;
+  while (true) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+    if (v) break;
+    __nanosleep(64);
+  }
 }
 
 // Launch helper: instantiate a kernel template for C's storage datatype.

@@ -76,7 +76,7 @@ struct GemmDesc {
   int64_t me, ne, ke;
   DEpilogue epi;
   int32_t exact_mode;
-  int32_t reserved;
+  int32_t sk_grid;     // fast kernels: > 0 = stream-K grid of that many CTAs (common.cuh: make_sched)
   int64_t kc;          // EXACT_BLOCK_COMBINE block length (real inner steps)
   double seed_beta;    // EXACT_DIRECT_SEEDED: beta as passed to gemm_ukr
   DView flat;          // EXACT_ONEM_MIXED: real_flatten(C) of the 1m variant
@@ -84,8 +84,19 @@ struct GemmDesc {
   int32_t splits;      // split-K factor of the fast kernels (1 = none)
   int32_t kb_per_split;  // 16-deep k-blocks per split
   int32_t prefetch;    // fast kernels: L2 prefetch distance in k-blocks ahead of the ring (0 = off)
-  void* partials;     // splits > 1: per (tile, split) accumulator tiles, comp precision
+  void* partials;      // splits > 1: per (tile, split) accumulator tiles, comp precision
+  unsigned long long* trace;  // tuning only (MDGEMM_TRACE): TRACE_WORDS stamps per CTA
+  void* sk_partials;   // stream-K: sk_grid partial tiles in thread-fragment order, comp precision
+  int* sk_flags;       // stream-K: sk_grid publish flags, zeroed before the launch
 };
+
+// Stream-K hybrid grid (common.cuh: make_sched): (tiles / G - 1) * G whole
+// tiles, then G CTAs sharing the rest.
+inline __host__ __device__ int64_t sk_launch_grid(int64_t tiles, int64_t G) { return (tiles / G - 1) * G + G; }
+
+// Per-CTA timeline for the tuning trace: {smid, start, first stage ready,
+// mainloop end, end} (%globaltimer nanoseconds).
+constexpr int TRACE_WORDS = 5;
 
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);

@@ -13,7 +13,9 @@
 // k loop the ring is reused for the fused typecast-accumulate epilogue
 // (fast_epilogue: accumulate_element semantics, kernels.cpp:79-95), which
 // moves C through shared memory with TMA bulk copies.  The kernel is
-// instantiated per C storage datatype (CDT) so the epilogue stays small.
+// instantiated per C storage datatype (CDT) so the epilogue stays small.  A
+// CTA works through the segment list of common.cuh (one tile, a split-K
+// slice, or a stream-K range).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -26,6 +28,7 @@ struct DmmaCfg {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
   static constexpr int BK = 16;
   static constexpr int NCW = WM * WN;
+  static constexpr int NCT = NCW * 32;
   static constexpr int THREADS = (NCW + 1) * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int MT = WTM / 8, NT = WTN / 8;
@@ -35,7 +38,8 @@ struct DmmaCfg {
   // C chunks of at least half the tile
   static constexpr size_t EPI_BYTES = size_t(BM) * BN * sizeof(double) * 3 / 2;
   static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
-  static constexpr size_t SMEM = REGION + (2 * STAGES + 1) * sizeof(uint64_t);
+  // full[STAGES], empty[STAGES], C-chunk barrier, segment-done barrier
+  static constexpr size_t SMEM = REGION + (2 * STAGES + 2) * sizeof(uint64_t);
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "warp tile must be a multiple of 8x8");
 };
 
@@ -45,57 +49,62 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <class C, int CDT>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc d) {
+template <class C, int CDT, bool SK>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __grid_constant__ GemmDesc d) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* sA = reinterpret_cast<double*>(smem);
   double* sB = sA + C::STAGES * C::STAGE_A;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::REGION);
   uint64_t* empty = full + C::STAGES;
   uint64_t* cbar = empty + C::STAGES;  // C-chunk load completion
+  uint64_t* segdone = cbar + 1;        // consumers finished an epilogue: the ring may be refilled
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
-  const int split = static_cast<int>(blockIdx.x / tiles);  // split-K slice of this CTA
-  const int64_t tile_id = blockIdx.x % tiles;
-  int tm, tn;
-  tile_coords(tile_id, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
-  const int nk_all = static_cast<int>(lpad / C::BK);
-  const int kb0 = d.splits > 1 ? split * d.kb_per_split : 0;
-  const int nk = d.splits > 1 ? min(nk_all - kb0, d.kb_per_split) : nk_all;
-  const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad +
-                     static_cast<int64_t>(kb0) * C::STAGE_A;
-  const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad +
-                     static_cast<int64_t>(kb0) * C::STAGE_B;
+  const Sched sc = make_sched<SK>(d, tiles, static_cast<int>(lpad / C::BK));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned long long t_start = d.trace ? globaltimer() : 0;
+  unsigned long long t_first = 0, t_loop = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
     mbar_init(cbar, 1);
+    mbar_init(segdone, 1);
     mbar_fence_init();
   }
   __syncthreads();
 
   if (warp == C::NCW) {  // ---------------- producer
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        if (d.prefetch > 0 && kb + d.prefetch < nk) {
-          const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
-          bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(double));
-          bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(double));
+      int it = 0, epis = 0;
+      bool after_epilogue = false;
+      for (int si = 0; si < sc.nseg; ++si) {
+        const Seg sg = sched_seg<SK>(sc, d, si);
+        if (after_epilogue) mbar_wait(segdone, (epis++) & 1);  // the epilogue reused the ring's memory
+        int tm, tn;
+        tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
+        const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
+        for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (d.prefetch > 0 && kb + d.prefetch < sg.k1) {
+            const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
+            bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(double));
+            bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(double));
+          }
+          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(double));
+          bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A, C::STAGE_A * sizeof(double),
+                   &full[s]);
+          bulk_g2s(sB + s * C::STAGE_B, Bg + static_cast<int64_t>(kb) * C::STAGE_B, C::STAGE_B * sizeof(double),
+                   &full[s]);
         }
-        if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(double));
-        bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A,
-                 C::STAGE_A * sizeof(double), &full[s]);
-        bulk_g2s(sB + s * C::STAGE_B, Bg + static_cast<int64_t>(kb) * C::STAGE_B,
-                 C::STAGE_B * sizeof(double), &full[s]);
+        after_epilogue = sg.kind == SEG_FULL || sg.kind == SEG_END;
       }
     }
     return;
@@ -104,81 +113,128 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(GemmDesc
   // ------------------------------------------------------------ consumers
   const int wm = warp % C::WM, wn = warp / C::WM;
   const int g = lane >> 2, tig = lane & 3;
-  double acc[C::MT][C::NT][2];
-#pragma unroll
-  for (int i = 0; i < C::MT; ++i)
-#pragma unroll
-    for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
+  const int tid = threadIdx.x;
   // (Register-double-buffered fragments do not fit: 10 warps per SM leave
   // 168 registers per thread and the 64x32 warp tile's accumulators take 128.)
   const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
   const double* a_base = sA + wm * C::WTM + g + tig * C::BM;
   const double* b_base = sB + wn * C::WTN + g + tig * C::BN;
-  for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % C::STAGES;
-    mbar_wait_u32(full_u + 8 * s, (kb / C::STAGES) & 1);
-    const double* a = a_base + s * C::STAGE_A;
-    const double* b = b_base + s * C::STAGE_B;
-#pragma unroll
-    for (int kk = 0; kk < C::BK; kk += 4) {
-      double af[C::MT], bf[C::NT];
-#pragma unroll
-      for (int i = 0; i < C::MT; ++i) af[i] = a[kk * C::BM + i * 8];
-#pragma unroll
-      for (int j = 0; j < C::NT; ++j) bf[j] = b[kk * C::BN + j * 8];
+  uint32_t cphase = 0;
+  int it = 0;
+  for (int si = 0; si < sc.nseg; ++si) {
+    const Seg sg = sched_seg<SK>(sc, d, si);
+    double acc[C::MT][C::NT][2];
+    if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      const int prev = sk_index(d, tiles) - 1;
+      if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
+      named_sync(1, C::NCT);
+      const double* slot = static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(prev) * (C::BM * C::BN);
 #pragma unroll
       for (int i = 0; i < C::MT; ++i)
 #pragma unroll
-        for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < C::NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) acc[i][j][h] = __ldcg(slot + ((i * C::NT + j) * 2 + h) * C::NCT + tid);
+    } else {
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
-    // generic-proxy reads of the stage before its async-proxy (TMA) refill
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
-  }
 
-  // ------------------------------------------------------------ epilogue
-  constexpr int NCT = C::NCW * 32;
-  if (d.splits > 1) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
-    double* part = static_cast<double*>(d.partials) + (split * tiles + tile_id) * (C::BM * C::BN);
+    for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait_u32(full_u + 8 * s, (it / C::STAGES) & 1);
+      if (d.trace && it == 0) t_first = globaltimer();
+      const double* a = a_base + s * C::STAGE_A;
+      const double* b = b_base + s * C::STAGE_B;
 #pragma unroll
-    for (int i = 0; i < C::MT; ++i)
+      for (int kk = 0; kk < C::BK; kk += 4) {
+        double af[C::MT], bf[C::NT];
 #pragma unroll
-      for (int j = 0; j < C::NT; ++j) {
-        const int r = wm * C::WTM + i * 8 + g;
-        const int c = wn * C::WTN + j * 8 + 2 * tig;
-        part[c * C::BM + r] = acc[i][j][0];
-        part[(c + 1) * C::BM + r] = acc[i][j][1];
+        for (int i = 0; i < C::MT; ++i) af[i] = a[kk * C::BM + i * 8];
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) bf[j] = b[kk * C::BN + j * 8];
+#pragma unroll
+        for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
-    return;
+      // generic-proxy reads of the stage before its async-proxy (TMA) refill
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
+    }
+    if (d.trace) t_loop = globaltimer();
+
+    if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
+      const int self = sk_index(d, tiles);
+      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN);
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) __stcg(slot + ((i * C::NT + j) * 2 + h) * C::NCT + tid, acc[i][j][h]);
+      __threadfence();
+      named_sync(1, C::NCT);
+      if (tid == 0) flag_release(d.sk_flags + self);
+      continue;
+    }
+    int tm, tn;
+    tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+    if (!SK && sg.kind == SEG_SPLIT) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
+      const int split = static_cast<int>(blockIdx.x / tiles);
+      double* part = static_cast<double*>(d.partials) + (split * tiles + sg.tile) * (C::BM * C::BN);
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+          const int r = wm * C::WTM + i * 8 + g;
+          const int c = wn * C::WTN + j * 8 + 2 * tig;
+          part[c * C::BM + r] = acc[i][j][0];
+          part[(c + 1) * C::BM + r] = acc[i][j][1];
+        }
+      continue;
+    }
+    named_sync(1, C::NCT);  // every consumer is done with the ring
+    // Stream-K: read the epilogue parameters through an opaque pointer so the
+    // compiler cannot hoist them out of the segment loop (they would stay
+    // live through the mainloop and push it into spills).
+    const DEpilogue* ep = &d.epi;
+    if (SK) asm volatile("" : "+l"(ep));
+    fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, *ep, static_cast<int64_t>(tm) * C::BM,
+                       static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, tid, C::NCT, cphase, [&](auto&& put) {
+#pragma unroll
+                         for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+                           for (int j = 0; j < C::NT; ++j) {
+                             const int r = wm * C::WTM + i * 8 + g;
+                             const int c = wn * C::WTN + j * 8 + 2 * tig;
+                             put(r, c, acc[i][j][0]);
+                             put(r, c + 1, acc[i][j][1]);
+                           }
+                       });
+    if (si + 1 < sc.nseg) {  // hand the shared memory back to the producer
+      fence_proxy_async();
+      named_sync(1, C::NCT);
+      if (tid == 0) mbar_arrive(segdone);
+    }
   }
-  named_sync(1, NCT);  // every consumer is done with the ring
-  fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
-                     static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, threadIdx.x, NCT, [&](auto&& put) {
-#pragma unroll
-                       for (int i = 0; i < C::MT; ++i)
-#pragma unroll
-                         for (int j = 0; j < C::NT; ++j) {
-                           const int r = wm * C::WTM + i * 8 + g;
-                           const int c = wn * C::WTN + j * 8 + 2 * tig;
-                           put(r, c, acc[i][j][0]);
-                           put(r, c + 1, acc[i][j][1]);
-                         }
-                     });
+  if (d.trace && tid == 0) trace_stamp(d.trace, t_start, t_first, t_loop);
 }
 
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
+  const int64_t grid = d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
   cudaError_t e = cudaSuccess;
   MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
-    e = cudaFuncSetAttribute(gemm_dmma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(C::SMEM));
+    auto kern = d.sk_grid > 0 ? gemm_dmma_kernel<C, CDT, true> : gemm_dmma_kernel<C, CDT, false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
-    gemm_dmma_kernel<C, CDT><<<static_cast<unsigned>(tiles * (d.splits > 1 ? d.splits : 1)), C::THREADS, C::SMEM,
-                               s>>>(d);
+    kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(d);
   });
   return cudaGetLastError();
 }
@@ -198,13 +254,10 @@ FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms) {
     if (t == 64128) return FastTile{64, 128, 16};
   }
   // 64x128 tiles, two CTAs per SM (measured better than 128x128 at every
-  // BASELINE shape), once they fill the machine evenly; 64x64 (three per SM)
-  // for small problems.
+  // BASELINE shape), once they fill one wave (the driver runs a partial last
+  // wave as stream-K); 64x64 (three per SM) for small problems.
   const int64_t pair = ((me + 63) / 64) * ((ne + 127) / 128);
-  const int64_t small = ((me + 63) / 64) * ((ne + 63) / 64);
-  const double eff_pair = double(pair) / (double((pair + 2 * sms - 1) / (2 * sms)) * 2 * sms);
-  const double eff_small = double(small) / (double((small + 3 * sms - 1) / (3 * sms)) * 3 * sms);
-  return pair >= 2LL * sms && eff_pair >= 0.9 * eff_small ? FastTile{64, 128, 16} : FastTile{64, 64, 16};
+  return pair >= 2LL * sms ? FastTile{64, 128, 16} : FastTile{64, 64, 16};
 }
 
 cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s) {

@@ -11,7 +11,8 @@
 // (fma.rn.f32x2 -> SASS FFMA2, A's element broadcast into both lanes), which
 // halves the issue slots of the outer product.  The fused typecast-accumulate
 // epilogue (fast_epilogue) follows; the kernel is instantiated per C
-// storage datatype.
+// storage datatype.  A CTA works through the segment list of common.cuh
+// (one tile, a split-K slice, or a stream-K range).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -33,61 +34,67 @@ struct FfmaCfg {
   // C chunks of at least half the tile
   static constexpr size_t EPI_BYTES = size_t(BM) * BN * sizeof(double) * 3 / 2;
   static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
-  static constexpr size_t SMEM = REGION + (2 * STAGES + 1) * sizeof(uint64_t);
+  // full[STAGES], empty[STAGES], C-chunk barrier, segment-done barrier
+  static constexpr size_t SMEM = REGION + (2 * STAGES + 2) * sizeof(uint64_t);
   static_assert(NCT % 32 == 0, "compute threads must be whole warps");
 };
 
-template <class C, int CDT>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc d) {
+template <class C, int CDT, bool SK>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __grid_constant__ GemmDesc d) {
   extern __shared__ __align__(128) unsigned char smem[];
   float* sA = reinterpret_cast<float*>(smem);
   float* sB = sA + C::STAGES * C::STAGE_A;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::REGION);
   uint64_t* empty = full + C::STAGES;
   uint64_t* cbar = empty + C::STAGES;  // C-chunk load completion
+  uint64_t* segdone = cbar + 1;        // consumers finished an epilogue: the ring may be refilled
 
   const int tiles_m = static_cast<int>((d.me + C::BM - 1) / C::BM);
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
-  const int split = static_cast<int>(blockIdx.x / tiles);  // split-K slice of this CTA
-  const int64_t tile_id = blockIdx.x % tiles;
-  int tm, tn;
-  tile_coords(tile_id, tiles_m, tiles_n, d.group_rows, tm, tn);
   const int64_t lpad = d.a.lpad;
-  const int nk_all = static_cast<int>(lpad / C::BK);
-  const int kb0 = d.splits > 1 ? split * d.kb_per_split : 0;
-  const int nk = d.splits > 1 ? min(nk_all - kb0, d.kb_per_split) : nk_all;
-  const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad +
-                    static_cast<int64_t>(kb0) * C::STAGE_A;
-  const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad +
-                    static_cast<int64_t>(kb0) * C::STAGE_B;
+  const Sched sc = make_sched<SK>(d, tiles, static_cast<int>(lpad / C::BK));
 
   const int tid = threadIdx.x;
+  const unsigned long long t_start = d.trace ? globaltimer() : 0;
+  unsigned long long t_first = 0, t_loop = 0;
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], C::NCW);
     }
     mbar_init(cbar, 1);
+    mbar_init(segdone, 1);
     mbar_fence_init();
   }
   __syncthreads();
 
   if (tid >= C::NCT) {  // ---------------- producer warp
     if (tid == C::NCT) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        if (d.prefetch > 0 && kb + d.prefetch < nk) {
-          const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
-          bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(float));
-          bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(float));
+      int it = 0, epis = 0;
+      bool after_epilogue = false;
+      for (int si = 0; si < sc.nseg; ++si) {
+        const Seg sg = sched_seg<SK>(sc, d, si);
+        if (after_epilogue) mbar_wait(segdone, (epis++) & 1);  // the epilogue reused the ring's memory
+        int tm, tn;
+        tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
+        const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
+        for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (d.prefetch > 0 && kb + d.prefetch < sg.k1) {
+            const int64_t pk = static_cast<int64_t>(kb + d.prefetch);
+            bulk_prefetch_l2(Ag + pk * C::STAGE_A, C::STAGE_A * sizeof(float));
+            bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(float));
+          }
+          if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(float));
+          bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A, C::STAGE_A * sizeof(float),
+                   &full[s]);
+          bulk_g2s(sB + s * C::STAGE_B, Bg + static_cast<int64_t>(kb) * C::STAGE_B, C::STAGE_B * sizeof(float),
+                   &full[s]);
         }
-        if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(float));
-        bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A,
-                 C::STAGE_A * sizeof(float), &full[s]);
-        bulk_g2s(sB + s * C::STAGE_B, Bg + static_cast<int64_t>(kb) * C::STAGE_B,
-                 C::STAGE_B * sizeof(float), &full[s]);
+        after_epilogue = sg.kind == SEG_FULL || sg.kind == SEG_END;
       }
     }
     return;
@@ -99,87 +106,130 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(GemmDesc
   // per inner step cost 32 issue slots.
   const int tx = tid % C::TXN, ty = tid / C::TXN;
   const int lane = tid & 31;
-  uint64_t acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
-
   const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
   const float* a_base = sA + ty * 4;
   const float* b_base = sB + tx * 4;
-  for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % C::STAGES;
-    mbar_wait_u32(full_u + 8 * s, (kb / C::STAGES) & 1);
-    const float* a = a_base + s * C::STAGE_A;
-    const float* b = b_base + s * C::STAGE_B;
-#pragma unroll
-    for (int kk = 0; kk < C::BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(a + kk * C::BM);
-      const float4 a1 = *reinterpret_cast<const float4*>(a + kk * C::BM + C::BM / 2);
-      const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN);
-      const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN + C::BN / 2);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const uint64_t bp[4] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        uint64_t ai;
-        asm("mov.b64 %0, {%1, %1};" : "=l"(ai) : "f"(av[i]));
-#pragma unroll
-        for (int p = 0; p < 4; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][p]) : "l"(ai), "l"(bp[p]));
-      }
-    }
-    // The stage was read through the generic proxy (LDS); the producer's next
-    // TMA write into it goes through the async proxy.  Order the two before
-    // releasing the slot (without this fence the refill can land before the
-    // reads complete: a cross-proxy WAR race).
-    fence_proxy_async();
-    __syncwarp();
-    if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
-  }
-
-  // ------------------------------------------------------------ epilogue
-  if (d.splits > 1) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
-    float* part = static_cast<float*>(d.partials) + (split * tiles + tile_id) * (C::BM * C::BN);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
-      float v[8];
+  uint32_t cphase = 0;
+  int it = 0;
+  for (int si = 0; si < sc.nseg; ++si) {
+    const Seg sg = sched_seg<SK>(sc, d, si);
+    uint64_t acc[8][4];
+    if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      const int prev = sk_index(d, tiles) - 1;
+      if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
+      named_sync(1, C::NCT);
+      const uint64_t* slot =
+          static_cast<const uint64_t*>(d.sk_partials) + static_cast<int64_t>(prev) * (C::BM * C::BN / 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        v[i] = __uint_as_float(static_cast<uint32_t>((j & 1) ? (acc[i][j >> 1] >> 32) : acc[i][j >> 1]));
-      *reinterpret_cast<float4*>(&part[c * C::BM + ty * 4]) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(&part[c * C::BM + C::BM / 2 + ty * 4]) = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[i][p] = __ldcg(slot + (i * 4 + p) * C::NCT + tid);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
     }
-    return;
-  }
-  named_sync(1, C::NCT);  // every consumer is done with the ring
-  fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, d.epi, static_cast<int64_t>(tm) * C::BM,
-                     static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, tid, C::NCT, [&](auto&& put) {
+
+    for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+      const int s = it % C::STAGES;
+      mbar_wait_u32(full_u + 8 * s, (it / C::STAGES) & 1);
+      if (d.trace && it == 0) t_first = globaltimer();
+      const float* a = a_base + s * C::STAGE_A;
+      const float* b = b_base + s * C::STAGE_B;
 #pragma unroll
-                       for (int i = 0; i < 8; ++i) {
-                         const int r = i < 4 ? ty * 4 + i : C::BM / 2 + ty * 4 + (i - 4);
+      for (int kk = 0; kk < C::BK; ++kk) {
+        const float4 a0 = *reinterpret_cast<const float4*>(a + kk * C::BM);
+        const float4 a1 = *reinterpret_cast<const float4*>(a + kk * C::BM + C::BM / 2);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(b + kk * C::BN + C::BN / 2);
+        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint64_t bp[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-                         for (int j = 0; j < 8; ++j) {
-                           const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
-                           const uint64_t v = acc[i][j >> 1];
-                           put(r, c, __uint_as_float(static_cast<uint32_t>((j & 1) ? (v >> 32) : v)));
+        for (int i = 0; i < 8; ++i) {
+          uint64_t ai;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(ai) : "f"(av[i]));
+#pragma unroll
+          for (int p = 0; p < 4; ++p) asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i][p]) : "l"(ai), "l"(bp[p]));
+        }
+      }
+      // The stage was read through the generic proxy (LDS); the producer's next
+      // TMA write into it goes through the async proxy.  Order the two before
+      // releasing the slot (without this fence the refill can land before the
+      // reads complete: a cross-proxy WAR race).
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
+    }
+    if (d.trace) t_loop = globaltimer();
+
+    if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
+      const int self = sk_index(d, tiles);
+      uint64_t* slot = static_cast<uint64_t*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN / 2);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) __stcg(slot + (i * 4 + p) * C::NCT + tid, acc[i][p]);
+      __threadfence();
+      named_sync(1, C::NCT);
+      if (tid == 0) flag_release(d.sk_flags + self);
+      continue;
+    }
+    int tm, tn;
+    tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+    if (!SK && sg.kind == SEG_SPLIT) {  // split-K: this CTA's partial tile, column-major, for the reduce pass
+      const int split = static_cast<int>(blockIdx.x / tiles);
+      float* part = static_cast<float*>(d.partials) + (split * tiles + sg.tile) * (C::BM * C::BN);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[i] = __uint_as_float(static_cast<uint32_t>((j & 1) ? (acc[i][j >> 1] >> 32) : acc[i][j >> 1]));
+        *reinterpret_cast<float4*>(&part[c * C::BM + ty * 4]) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(&part[c * C::BM + C::BM / 2 + ty * 4]) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+      continue;
+    }
+    named_sync(1, C::NCT);  // every consumer is done with the ring
+    // Stream-K: epilogue parameters through an opaque pointer (no hoisting
+    // out of the segment loop, see gemm_dmma.cu).
+    const DEpilogue* ep = &d.epi;
+    if (SK) asm volatile("" : "+l"(ep));
+    fast_epilogue<CDT>(smem, static_cast<uint32_t>(C::REGION), cbar, *ep, static_cast<int64_t>(tm) * C::BM,
+                       static_cast<int64_t>(tn) * C::BN, C::BM, C::BN, tid, C::NCT, cphase, [&](auto&& put) {
+#pragma unroll
+                         for (int i = 0; i < 8; ++i) {
+                           const int r = i < 4 ? ty * 4 + i : C::BM / 2 + ty * 4 + (i - 4);
+#pragma unroll
+                           for (int j = 0; j < 8; ++j) {
+                             const int c = j < 4 ? tx * 4 + j : C::BN / 2 + tx * 4 + (j - 4);
+                             const uint64_t v = acc[i][j >> 1];
+                             put(r, c, __uint_as_float(static_cast<uint32_t>((j & 1) ? (v >> 32) : v)));
+                           }
                          }
-                       }
-                     });
+                       });
+    if (si + 1 < sc.nseg) {  // hand the shared memory back to the producer
+      fence_proxy_async();
+      named_sync(1, C::NCT);
+      if (tid == 0) mbar_arrive(segdone);
+    }
+  }
+  if (d.trace && tid == 0) trace_stamp(d.trace, t_start, t_first, t_loop);
 }
 
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
+  const int64_t grid = d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
   cudaError_t e = cudaSuccess;
   MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
-    e = cudaFuncSetAttribute(gemm_ffma_kernel<C, CDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(C::SMEM));
+    auto kern = d.sk_grid > 0 ? gemm_ffma_kernel<C, CDT, true> : gemm_ffma_kernel<C, CDT, false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
     if (e != cudaSuccess) return e;
-    gemm_ffma_kernel<C, CDT><<<static_cast<unsigned>(tiles * (d.splits > 1 ? d.splits : 1)), C::THREADS, C::SMEM,
-                               s>>>(d);
+    kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(d);
   });
   return cudaGetLastError();
 }

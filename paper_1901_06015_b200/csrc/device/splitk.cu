@@ -30,8 +30,9 @@ __global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(GemmDesc d, 
   const int elems = BM * BN;
   const AccT* base = static_cast<const AccT*>(d.partials) + tile_id * elems;
   const int64_t stride = tiles * elems;
+  uint32_t cphase = 0;
   fast_epilogue<CDT>(smem, region, cbar, d.epi, static_cast<int64_t>(tm) * BM, static_cast<int64_t>(tn) * BN, BM, BN,
-                     threadIdx.x, RED_THREADS, [&](auto&& put) {
+                     threadIdx.x, RED_THREADS, cphase, [&](auto&& put) {
                        for (int e = threadIdx.x; e < elems; e += RED_THREADS) {
                          AccT s = base[e];
                          for (int sp = 1; sp < d.splits; ++sp) s = s + base[sp * stride + e];

@@ -185,6 +185,10 @@ std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Da
 }
 
 void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc) {
+  execute_scheduled(p, numerics, stream_ptr, fc, false);
+}
+
+void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (p.m == 0 || p.n == 0) return;
   // Device-ordered entry points need device operands; a host pointer here
@@ -232,14 +236,30 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
     kb_per_split = static_cast<int>((nk + splits - 1) / splits);
     splits = static_cast<int>((nk + kb_per_split - 1) / kb_per_split);
   }
+  // Stream-K when whole tiles would leave the last wave partly empty: the
+  // tiles x k-blocks are cut into one equal range per CTA slot (common.cuh:
+  // make_sched); bitwise identical to the classic grid.
+  const int64_t slots = static_cast<int64_t>(sms) * per_sm;
+  int sk_grid = 0;
+  if (!exact && splits == 1 && tiles > slots && tile.bn == 128) {
+    const int64_t waves = (tiles + slots - 1) / slots;
+    const double eff = static_cast<double>(tiles) / static_cast<double>(waves * slots);
+    int mode = 0;  // tuning override MDGEMM_STREAMK: 0 auto, 1 force on, -1 off
+    if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
+    if (mode > 0 || (mode == 0 && !shared && eff < 0.97)) sk_grid = static_cast<int>(slots);
+  }
   const size_t acc_size = single ? sizeof(float) : sizeof(double);
   const size_t off_b = (pa.bytes + 255) / 256 * 256;
   const size_t off_p = off_b + (pb.bytes + 255) / 256 * 256;
-  const size_t part_bytes = splits > 1 ? static_cast<size_t>(splits * tiles * tile.bm * tile.bn) * acc_size : 0;
+  const size_t part_bytes = splits > 1 ? static_cast<size_t>(splits * tiles * tile.bm * tile.bn) * acc_size
+                                       : static_cast<size_t>(sk_grid) * tile.bm * tile.bn * acc_size;
+  const size_t off_f = off_p + (part_bytes + 255) / 256 * 256;
+  const size_t flag_bytes = static_cast<size_t>(sk_grid) * sizeof(int);
   void* ws = nullptr;
-  cuda_check(cudaMallocAsync(&ws, off_p + part_bytes, st), "workspace allocation");
+  cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
   char* wsa = static_cast<char*>(ws);
-  cudaError_t err;
+  cudaError_t err = sk_grid > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
+  cuda_check(err, "stream-K flags");
   {
     prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes));
     err = mdg::launch_pack(pa.desc, wsa, st);
@@ -270,6 +290,9 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   g.splits = splits;
   g.kb_per_split = kb_per_split;
   g.partials = splits > 1 ? wsa + off_p : nullptr;
+  g.sk_grid = sk_grid;
+  g.sk_partials = sk_grid > 0 ? wsa + off_p : nullptr;
+  g.sk_flags = sk_grid > 0 ? reinterpret_cast<int*>(wsa + off_f) : nullptr;
   g.prefetch = 0;
   if (const char* force = std::getenv("MDGEMM_PREFETCH")) g.prefetch = std::atoi(force);
 
@@ -296,9 +319,31 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
       err = mdg::launch_gemm_exact(g, single, st);
     } else {
       const int kind = single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA;
+      const char* trace_path = std::getenv("MDGEMM_TRACE");  // tuning: per-CTA timeline of every gemm kernel
+      const int64_t grid = sk_grid > 0 ? mdg::sk_launch_grid(tiles, sk_grid) : tiles * splits;
+      if (trace_path && grid > 0 && err == cudaSuccess)
+        err = cudaMallocAsync(reinterpret_cast<void**>(&g.trace), grid * mdg::TRACE_WORDS * 8, st);
       {
         prof::Scope scope(kind, st, 2.0 * p.m * p.n * p.k);
-        err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+        if (err == cudaSuccess)
+          err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+      }
+      if (g.trace) {
+        std::vector<unsigned long long> h(static_cast<size_t>(grid) * mdg::TRACE_WORDS);
+        if (err == cudaSuccess)
+          err = cudaMemcpyAsync(h.data(), g.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+        if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+        cudaFreeAsync(g.trace, st);
+        g.trace = nullptr;
+        if (FILE* f = std::fopen(trace_path, "a")) {
+          std::fprintf(f, "K %s %lld %lld %lld %d %d %d %lld\n", single ? "ffma" : "dmma", (long long)p.m,
+                       (long long)p.n, (long long)p.k, tile.bm, tile.bn, splits, (long long)grid);
+          for (int64_t b = 0; b < grid; ++b) {
+            const unsigned long long* r = &h[static_cast<size_t>(b) * mdg::TRACE_WORDS];
+            std::fprintf(f, "%llu %llu %llu %llu %llu\n", r[0], r[1], r[2], r[3], r[4]);
+          }
+          std::fclose(f);
+        }
       }
       if (err == cudaSuccess && splits > 1) {
         prof::Scope scope(kind, st, 0.0);  // same job: its time counts against the gemm's flops

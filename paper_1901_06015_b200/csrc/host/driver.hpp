@@ -39,6 +39,12 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
                               Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
                               void* stream);
 
+// execute() with the scheduling hint of the batch runner: `shared` = other
+// calls of the same batch may run concurrently on the device, so the kernel
+// keeps the hardware-scheduled classic grid (whose waves interleave with the
+// neighbours') instead of a stream-K tail sized for an idle GPU.
+void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared);
+
 // The value the reference's FlopCounter reaches for this plan.
 uint64_t reference_flops(const ExecutionPlan& p);
 

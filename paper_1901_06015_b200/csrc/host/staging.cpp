@@ -211,7 +211,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
         if (s != c.stream && latest[s] >= 0)
           cuda_check(cudaStreamWaitEvent(cst, cs[static_cast<size_t>(latest[s])].comp_done, 0), "dependency");
 
-      execute(p, cfg.numerics, cst, fc);
+      execute_scheduled(p, cfg.numerics, cst, fc, cs.size() > 1);
       cuda_check(cudaEventRecord(c.comp_done, cst), "event");
 
       // ---- copy-out of a host C, release of staging
