@@ -425,10 +425,13 @@ __device__ __forceinline__ void tile_coords(int64_t id, int tiles_m, int tiles_n
 // Classic grid: one segment, the whole k range of tile blockIdx % tiles (or
 // split-K slice blockIdx / tiles of it).
 //
-// Stream-K grid (d.sk_grid = G CTAs, all resident): the tiles x nk k-blocks
-// are cut into G equal contiguous ranges, CTA b owning [b U/G, (b+1) U/G).
-// A range ends inside a tile at most once on each side (ranges are >= one
-// tile long), giving up to three kinds of segment:
+// Stream-K hybrid grid (d.sk_grid = G, the resident CTA slots): with
+// R = tiles % G > 0, the first dp = (tiles / G - 1) G CTAs take one whole tile
+// each (hardware-scheduled waves, as in the classic grid) and the last G CTAs
+// cut the remaining G + R tiles x nk k-blocks into G equal contiguous ranges,
+// CTA b owning [b U/G, (b+1) U/G) of them.  A range is at least one tile
+// long, so it ends inside a tile at most once on each side, giving up to
+// three kinds of segment:
 //   SEG_START  the first k-blocks of the tile the range ends in: accumulated
 //              from zero and published to partial slot b (run FIRST, so the
 //              next CTA never waits long);
@@ -451,34 +454,31 @@ struct Seg {
 // register-bound kernel (tiles and k-blocks per launch are < 2^31).
 struct Sched {
   int tiles, nk, nseg;
+  int sk;                    // stream-K slot of this CTA (-1: a whole-tile CTA)
   int start_tile, start_k1;  // SEG_START (start_k1 == 0: none)
-  int full0;                 // first SEG_FULL tile
+  int full0;                 // first SEG_FULL tile (its range: [full0, start_tile))
   int end_tile, end_k0;      // SEG_END (end_k0 == 0: none)
 };
 
 // SK is a template flag so the classic kernels compile to one straight
-// segment (the stream-K loop costs registers).
+// segment (the segment loop costs registers).
 template <bool SK>
 __device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, int nk) {
   Sched s{};
   s.tiles = static_cast<int>(tiles);
   s.nk = nk;
-  if (!SK) {
-    s.nseg = 1;
-    return s;
-  }
-  // Hybrid grid: the first dp = (tiles / G - 1) * G CTAs take one whole tile
-  // each (hardware-scheduled waves, as in the classic grid); the last G CTAs
-  // share the remaining G + tiles % G tiles as equal k-block ranges.
-  const int64_t G = d.sk_grid;
-  const int64_t dp = (tiles / G - 1) * G;
-  if (static_cast<int64_t>(blockIdx.x) < dp) {
+  s.sk = -1;
+  s.nseg = 1;
+  if (!SK) return s;
+  const int64_t G = d.sk_grid, dp = sk_dp_tiles(tiles, G);
+  const int64_t b = static_cast<int64_t>(blockIdx.x) - dp;
+  if (b < 0) {  // a whole tile
     s.full0 = static_cast<int>(blockIdx.x);
     s.start_tile = s.full0 + 1;
-    s.nseg = 1;
     return s;
   }
-  const int64_t U = (tiles - dp) * nk, b = blockIdx.x - dp;
+  s.sk = static_cast<int>(b);
+  const int64_t U = (tiles - dp) * nk;
   const int64_t u0 = dp * nk + b * U / G, u1 = dp * nk + (b + 1) * U / G;
   s.start_tile = static_cast<int>(u1 / nk);
   s.start_k1 = static_cast<int>(u1 % nk);
@@ -487,11 +487,6 @@ __device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, in
   s.full0 = static_cast<int>((u0 + nk - 1) / nk);
   s.nseg = (s.start_k1 != 0) + (s.start_tile - s.full0) + (s.end_k0 != 0);
   return s;
-}
-
-// Stream-K CTA index among the last sk_grid CTAs (partial slots and flags).
-__device__ __forceinline__ int sk_index(const GemmDesc& d, int64_t tiles) {
-  return static_cast<int>(blockIdx.x - (tiles / d.sk_grid - 1) * d.sk_grid);
 }
 
 template <bool SK>

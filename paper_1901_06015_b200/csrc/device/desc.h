@@ -90,13 +90,19 @@ struct GemmDesc {
   int* sk_flags;       // stream-K: sk_grid publish flags, zeroed before the launch
 };
 
-// Stream-K hybrid grid (common.cuh: make_sched): (tiles / G - 1) * G whole
-// tiles, then G CTAs sharing the rest.
-inline __host__ __device__ int64_t sk_launch_grid(int64_t tiles, int64_t G) { return (tiles / G - 1) * G + G; }
+// Stream-K hybrid grid (common.cuh: make_sched): dp whole-tile CTAs, then G
+// CTAs sharing the last G + tiles % G tiles as k-block ranges.
+inline __host__ __device__ int64_t sk_dp_tiles(int64_t tiles, int64_t G) {
+  return tiles % G == 0 ? tiles : (tiles / G - 1) * G;
+}
+inline __host__ __device__ int64_t sk_launch_grid(int64_t tiles, int64_t G) {
+  return sk_dp_tiles(tiles, G) + (tiles % G == 0 ? 0 : G);
+}
 
 // Per-CTA timeline for the tuning trace: {smid, start, first stage ready,
 // mainloop end, end} (%globaltimer nanoseconds).
-constexpr int TRACE_WORDS = 5;
+// Word 5: the producer's first bulk-copy issue.
+constexpr int TRACE_WORDS = 6;
 
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);
@@ -112,6 +118,10 @@ FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms);
 FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms);
 cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
 cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
+// Resident CTAs per SM of the kernel a tile shape / C datatype launches
+// (occupancy query; sizes the split-K and stream-K grids).
+int dmma_ctas_per_sm(const FastTile& t, int cdt);
+int ffma_ctas_per_sm(const FastTile& t, int cdt);
 // Split-K: sum the `splits` partial tiles in split order and run the fused
 // epilogue (one CTA per tile).
 cudaError_t launch_splitk_reduce(const GemmDesc& d, const FastTile& t, bool single, cudaStream_t s);

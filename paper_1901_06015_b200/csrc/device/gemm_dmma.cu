@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
             bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(double));
           }
           if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          if (d.trace && it == 0) d.trace[static_cast<size_t>(blockIdx.x) * TRACE_WORDS + 5] = globaltimer();
           mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(double));
           bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A, C::STAGE_A * sizeof(double),
                    &full[s]);
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
     const Seg sg = sched_seg<SK>(sc, d, si);
     double acc[C::MT][C::NT][2];
     if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
-      const int prev = sk_index(d, tiles) - 1;
+      const int prev = sc.sk - 1;
       if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
       named_sync(1, C::NCT);
       const double* slot = static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(prev) * (C::BM * C::BN);
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
     if (d.trace) t_loop = globaltimer();
 
     if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
-      const int self = sk_index(d, tiles);
+      const int self = sc.sk;
       double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN);
 #pragma unroll
       for (int i = 0; i < C::MT; ++i)
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
                              put(r, c + 1, acc[i][j][1]);
                            }
                        });
-    if (si + 1 < sc.nseg) {  // hand the shared memory back to the producer
+    if (SK && si + 1 < sc.nseg) {  // hand the shared memory back to the producer
       fence_proxy_async();
       named_sync(1, C::NCT);
       if (tid == 0) mbar_arrive(segdone);
@@ -228,7 +229,8 @@ template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
-  const int64_t grid = d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
+  const int64_t grid =
+      d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
   cudaError_t e = cudaSuccess;
   MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
     auto kern = d.sk_grid > 0 ? gemm_dmma_kernel<C, CDT, true> : gemm_dmma_kernel<C, CDT, false>;
@@ -245,7 +247,26 @@ using Big = DmmaCfg<128, 128, 2, 4, 4>;
 using Pair = DmmaCfg<64, 128, 1, 4, 4, 2>;
 using Small = DmmaCfg<64, 64, 2, 2, 4>;
 
+template <class C>
+int ctas_per_sm(int cdt) {
+  int n = 0;
+  MDG_DISPATCH_CDT(cdt, CDT, {
+    if (cudaFuncSetAttribute(gemm_dmma_kernel<C, CDT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(C::SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gemm_dmma_kernel<C, CDT, false>, C::THREADS, C::SMEM) !=
+            cudaSuccess)
+      n = 1;
+  });
+  return n > 0 ? n : 1;
+}
+
 }  // namespace
+
+int dmma_ctas_per_sm(const FastTile& t, int cdt) {
+  if (t.bm == 128 && t.bn == 128) return ctas_per_sm<Big>(cdt);
+  if (t.bm == 64 && t.bn == 128) return ctas_per_sm<Pair>(cdt);
+  return ctas_per_sm<Small>(cdt);
+}
 
 FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms) {
   if (const char* force = std::getenv("MDGEMM_DMMA_TILE")) {  // tuning override: 64 | 128 | 64128

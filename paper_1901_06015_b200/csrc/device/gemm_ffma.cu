@@ -20,7 +20,7 @@
 namespace mdg {
 namespace {
 
-template <int BM_, int BN_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int STAGES_, int MINB_, int EPI_ESZ = 8>
 struct FfmaCfg {
   static constexpr int BM = BM_, BN = BN_, STAGES = STAGES_, MINB = MINB_;
   static constexpr int BK = 16;
@@ -30,9 +30,9 @@ struct FfmaCfg {
   static constexpr int THREADS = NCT + 32;
   static constexpr int STAGE_A = BK * BM, STAGE_B = BK * BN;  // floats
   static constexpr size_t RING_BYTES = size_t(STAGES) * (STAGE_A + STAGE_B) * sizeof(float);
-  // epilogue: the staged accumulator tile (<= 8 bytes per real element) plus
-  // C chunks of at least half the tile
-  static constexpr size_t EPI_BYTES = size_t(BM) * BN * sizeof(double) * 3 / 2;
+  // epilogue: the staged accumulator tile (EPI_ESZ = bytes per real element
+  // of C's storage) plus C chunks of at least half the tile
+  static constexpr size_t EPI_BYTES = size_t(BM) * BN * EPI_ESZ * 3 / 2;
   static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
   // full[STAGES], empty[STAGES], C-chunk barrier, segment-done barrier
   static constexpr size_t SMEM = REGION + (2 * STAGES + 2) * sizeof(uint64_t);
@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
             bulk_prefetch_l2(Bg + pk * C::STAGE_B, C::STAGE_B * sizeof(float));
           }
           if (it >= C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          if (d.trace && it == 0) d.trace[static_cast<size_t>(blockIdx.x) * TRACE_WORDS + 5] = globaltimer();
           mbar_arrive_expect_tx(&full[s], (C::STAGE_A + C::STAGE_B) * sizeof(float));
           bulk_g2s(sA + s * C::STAGE_A, Ag + static_cast<int64_t>(kb) * C::STAGE_A, C::STAGE_A * sizeof(float),
                    &full[s]);
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
     const Seg sg = sched_seg<SK>(sc, d, si);
     uint64_t acc[8][4];
     if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
-      const int prev = sk_index(d, tiles) - 1;
+      const int prev = sc.sk - 1;
       if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
       named_sync(1, C::NCT);
       const uint64_t* slot =
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
     if (d.trace) t_loop = globaltimer();
 
     if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
-      const int self = sk_index(d, tiles);
+      const int self = sc.sk;
       uint64_t* slot = static_cast<uint64_t*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN / 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
                            }
                          }
                        });
-    if (si + 1 < sc.nseg) {  // hand the shared memory back to the producer
+    if (SK && si + 1 < sc.nseg) {  // hand the shared memory back to the producer
       fence_proxy_async();
       named_sync(1, C::NCT);
       if (tid == 0) mbar_arrive(segdone);
@@ -219,26 +220,55 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
   if (d.trace && tid == 0) trace_stamp(d.trace, t_start, t_first, t_loop);
 }
 
+using Big = FfmaCfg<128, 128, 8, 1>;
+using Pair = FfmaCfg<64, 128, 8, 2>;  // two CTAs per SM: epilogues overlap mainloops
+// single-precision C: a 4-byte staging tile leaves room for three CTAs per SM
+using Pair3 = FfmaCfg<64, 128, 6, 3, 4>;
+using Small = FfmaCfg<64, 64, 6, 4>;
+
+// The configuration a tile shape runs with for C's storage datatype.
+template <class C, int CDT>
+using CfgFor = typename std::conditional<(C::BM == 64 && C::BN == 128 && (CDT == MDG_DT_S || CDT == MDG_DT_C)),
+                                         Pair3, C>::type;
+
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {
   const int64_t tiles = ((d.me + C::BM - 1) / C::BM) * ((d.ne + C::BN - 1) / C::BN);
   if (tiles == 0) return cudaSuccess;
-  const int64_t grid = d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
+  const int64_t grid =
+      d.sk_grid > 0 ? sk_launch_grid(tiles, d.sk_grid) : tiles * (d.splits > 1 ? d.splits : 1);
   cudaError_t e = cudaSuccess;
   MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
-    auto kern = d.sk_grid > 0 ? gemm_ffma_kernel<C, CDT, true> : gemm_ffma_kernel<C, CDT, false>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::SMEM));
+    using K = CfgFor<C, CDT>;
+    auto kern = d.sk_grid > 0 ? gemm_ffma_kernel<K, CDT, true> : gemm_ffma_kernel<K, CDT, false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(K::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, s>>>(d);
+    kern<<<static_cast<unsigned>(grid), K::THREADS, K::SMEM, s>>>(d);
   });
   return cudaGetLastError();
 }
 
-using Big = FfmaCfg<128, 128, 8, 1>;
-using Pair = FfmaCfg<64, 128, 8, 2>;  // two CTAs per SM: epilogues overlap mainloops
-using Small = FfmaCfg<64, 64, 6, 4>;
+template <class C>
+int ctas_per_sm(int cdt) {
+  int n = 0;
+  MDG_DISPATCH_CDT(cdt, CDT, {
+    using K = CfgFor<C, CDT>;
+    if (cudaFuncSetAttribute(gemm_ffma_kernel<K, CDT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(K::SMEM)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gemm_ffma_kernel<K, CDT, false>, K::THREADS, K::SMEM) !=
+            cudaSuccess)
+      n = 1;
+  });
+  return n > 0 ? n : 1;
+}
 
 }  // namespace
+
+int ffma_ctas_per_sm(const FastTile& t, int cdt) {
+  if (t.bm == 128 && t.bn == 128) return ctas_per_sm<Big>(cdt);
+  if (t.bm == 64 && t.bn == 128) return ctas_per_sm<Pair>(cdt);
+  return ctas_per_sm<Small>(cdt);
+}
 
 FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms) {
   if (const char* force = std::getenv("MDGEMM_FFMA_TILE")) {  // tuning override: 64 | 128 | 64128

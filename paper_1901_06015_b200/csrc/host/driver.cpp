@@ -7,6 +7,7 @@
 #include "profile.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -184,6 +185,20 @@ std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Da
   return pack_geometry(src, side, format, target, reg_block, 0).bytes;
 }
 
+// Resident CTAs per SM of a fast kernel (occupancy query, cached per
+// tile shape x kernel x C datatype; the value is the same on every B200).
+static int ctas_per_sm(const mdg::FastTile& t, bool single, int cdt) {
+  static std::atomic<int> cache[3][2][4] = {};
+  const int ti = t.bm == 128 ? 0 : (t.bn == 128 ? 1 : 2);
+  std::atomic<int>& slot = cache[ti][single ? 1 : 0][cdt & 3];
+  int v = slot.load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = single ? mdg::ffma_ctas_per_sm(t, cdt) : mdg::dmma_ctas_per_sm(t, cdt);
+    slot.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc) {
   execute_scheduled(p, numerics, stream_ptr, fc, false);
 }
@@ -228,7 +243,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   // Split-K when the tile grid cannot fill the machine (deterministic: the
   // partial tiles are summed in split order by the reduce pass).
   const int64_t tiles = ((p.m + tile.bm - 1) / tile.bm) * ((p.n + tile.bn - 1) / tile.bn);
-  const int per_sm = tile.bm == 64 && tile.bn == 128 ? 2 : (tile.bm == 64 && tile.bn == 64 ? 3 : 1);
+  const int per_sm = exact ? 1 : ctas_per_sm(tile, single, to_dview(p.c).dtype);
   const int64_t nk = lpad / tile.bk;
   int splits = exact ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
   int kb_per_split = static_cast<int>(nk);
@@ -236,17 +251,24 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     kb_per_split = static_cast<int>((nk + splits - 1) / splits);
     splits = static_cast<int>((nk + kb_per_split - 1) / kb_per_split);
   }
-  // Stream-K when whole tiles would leave the last wave partly empty: the
-  // tiles x k-blocks are cut into one equal range per CTA slot (common.cuh:
-  // make_sched); bitwise identical to the classic grid.
+  // Stream-K tail for a call that has the GPU to itself, when the classic
+  // grid's last wave would run mostly empty: whole-tile CTAs for all but the
+  // last full wave, then one CTA per slot sharing the rest as k-block ranges
+  // (common.cuh: make_sched); bitwise identical to the classic grid.
+  // Thresholds measured on B200 (cfg2 sizes): with two CTAs per SM (DMMA)
+  // it wins up to a tail wave 80 % full (+2..7 %); with three per SM (FFMA,
+  // single-precision C) the older CTAs of an SM get most issue slots, the
+  // static ranges wait for the slowest one, and it only wins for an almost
+  // empty tail (< 10 %).  Inside a concurrent batch the classic grid stays:
+  // its hardware-scheduled tiles interleave with the other calls' kernels.
   const int64_t slots = static_cast<int64_t>(sms) * per_sm;
   int sk_grid = 0;
-  if (!exact && splits == 1 && tiles > slots && tile.bn == 128) {
-    const int64_t waves = (tiles + slots - 1) / slots;
-    const double eff = static_cast<double>(tiles) / static_cast<double>(waves * slots);
+  if (!exact && splits == 1 && tiles > slots && tiles % slots != 0 && tile.bn == 128) {
     int mode = 0;  // tuning override MDGEMM_STREAMK: 0 auto, 1 force on, -1 off
     if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
-    if (mode > 0 || (mode == 0 && !shared && eff < 0.97)) sk_grid = static_cast<int>(slots);
+    const double tail = static_cast<double>(tiles % slots) / static_cast<double>(slots);
+    const bool wins = tail < (per_sm >= 3 ? 0.10 : 0.80);
+    if (mode > 0 || (mode == 0 && !shared && wins)) sk_grid = static_cast<int>(slots);
   }
   const size_t acc_size = single ? sizeof(float) : sizeof(double);
   const size_t off_b = (pa.bytes + 255) / 256 * 256;
@@ -254,7 +276,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   const size_t part_bytes = splits > 1 ? static_cast<size_t>(splits * tiles * tile.bm * tile.bn) * acc_size
                                        : static_cast<size_t>(sk_grid) * tile.bm * tile.bn * acc_size;
   const size_t off_f = off_p + (part_bytes + 255) / 256 * 256;
-  const size_t flag_bytes = static_cast<size_t>(sk_grid) * sizeof(int);
+  const size_t flag_bytes = static_cast<size_t>(sk_grid) * sizeof(int);  // stream-K publish flags
   void* ws = nullptr;
   cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
   char* wsa = static_cast<char*>(ws);
@@ -340,7 +362,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
                        (long long)p.n, (long long)p.k, tile.bm, tile.bn, splits, (long long)grid);
           for (int64_t b = 0; b < grid; ++b) {
             const unsigned long long* r = &h[static_cast<size_t>(b) * mdg::TRACE_WORDS];
-            std::fprintf(f, "%llu %llu %llu %llu %llu\n", r[0], r[1], r[2], r[3], r[4]);
+            std::fprintf(f, "%llu %llu %llu %llu %llu %llu\n", r[0], r[1], r[2], r[3], r[4], r[5]);
           }
           std::fclose(f);
         }

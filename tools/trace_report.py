@@ -27,6 +27,7 @@ def report(kn):
     t1 = max(r[4] for r in c)
     span = (t1 - t0) / 1e3
     fill = sum(r[2] - r[1] for r in c) / len(c) / 1e3
+    issue = sum(r[5] - r[1] for r in c if len(r) > 5 and r[5]) / len(c) / 1e3
     loop = sum(r[3] - r[2] for r in c) / len(c) / 1e3
     epi = sum(r[4] - r[3] for r in c) / len(c) / 1e3
     busy = sum(r[4] - r[1] for r in c) / 1e3
@@ -51,7 +52,7 @@ def report(kn):
     flops = 2.0 * kn["m"] * kn["n"] * kn["k"]
     print(f"{kn['kind']} {kn['m']}x{kn['n']}x{kn['k']} tile {kn['bm']}x{kn['bn']} splits {kn['splits']} grid {kn['grid']}"
           f" SMs {sms} slots/SM {slots}: span {span:.1f} us ({flops / span / 1e6:.1f} TF/s) |"
-          f" per CTA fill {fill:.2f} loop {loop:.1f} epi {epi:.2f} us |"
+          f" per CTA fill {fill:.2f} (first issue after {issue:.2f}) loop {loop:.1f} epi {epi:.2f} us |"
           f" slot occupancy {busy / (span * sms * slots):.3f} | first-wave start skew {(starts[min(len(starts)-1, sms*slots-1)] - t0)/1e3:.2f} us"
           f" | end-median->end {tail:.1f} us")
 
