@@ -303,6 +303,11 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Arrive on a named barrier without waiting (the producer warp's half of a
+// start-up handshake the consumers complete with named_sync).
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // --------------------------------------------------------- fused epilogue
 // The accumulator tile (BM x BN real-image values held in registers) meets C
@@ -408,16 +413,19 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
 // (8) makes concurrently running CTAs share A and B panels in L2 (long k);
 // a group spanning all tile-rows keeps the concurrent C tiles inside a few
 // column panels (short k, where C traffic dominates).
-__device__ __forceinline__ void tile_coords(int64_t id, int tiles_m, int tiles_n, int group_rows, int& tm,
+// 32-bit unsigned arithmetic (a launch has < 2^31 tiles): it runs in every
+// CTA's prologue, where a 64-bit division costs ~100 instructions.
+__device__ __forceinline__ void tile_coords(int64_t id64, int tiles_m, int tiles_n, int group_rows, int& tm,
                                             int& tn) {
-  const int GROUP = group_rows > 0 ? group_rows : 8;
-  const int64_t per_group = static_cast<int64_t>(GROUP) * tiles_n;
-  const int group = static_cast<int>(id / per_group);
-  const int first = group * GROUP;
-  const int gsize = min(tiles_m - first, GROUP);
-  const int64_t in = id % per_group;
-  tm = first + static_cast<int>(in % gsize);
+  const unsigned id = static_cast<unsigned>(id64);
+  const unsigned GROUP = static_cast<unsigned>(group_rows > 0 ? min(group_rows, tiles_m) : min(8, tiles_m));
+  const unsigned per_group = GROUP * static_cast<unsigned>(tiles_n);
+  const unsigned group = id / per_group;
+  const unsigned first = group * GROUP;
+  const unsigned gsize = min(static_cast<unsigned>(tiles_m) - first, GROUP);
+  const unsigned in = id - group * per_group;
   tn = static_cast<int>(in / gsize);
+  tm = static_cast<int>(first + (in - static_cast<unsigned>(tn) * gsize));
 }
 
 // ---- work schedule of one CTA of the fast kernels ------------------------

@@ -68,18 +68,20 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned long long t_start = d.trace ? globaltimer() : 0;
   unsigned long long t_first = 0, t_loop = 0;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NCW);
-    }
-    mbar_init(cbar, 1);
-    mbar_init(segdone, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
+  // The producer sets up the barriers and starts streaming without waiting
+  // for the consumers (see gemm_ffma.cu).
   if (warp == C::NCW) {  // ---------------- producer
+    if (lane == 0) {
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], C::NCW);
+      }
+      mbar_init(cbar, 1);
+      mbar_init(segdone, 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    named_arrive(2, C::THREADS);
     if (lane == 0) {
       int it = 0, epis = 0;
       bool after_epilogue = false;
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
   }
 
   // ------------------------------------------------------------ consumers
+  named_sync(2, C::THREADS);  // the producer has initialised the barriers
   const int wm = warp % C::WM, wn = warp / C::WM;
   const int g = lane >> 2, tig = lane & 3;
   const int tid = threadIdx.x;

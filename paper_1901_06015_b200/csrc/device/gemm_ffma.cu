@@ -58,18 +58,21 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
   const int tid = threadIdx.x;
   const unsigned long long t_start = d.trace ? globaltimer() : 0;
   unsigned long long t_first = 0, t_loop = 0;
-  if (tid == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NCW);
-    }
-    mbar_init(cbar, 1);
-    mbar_init(segdone, 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-
+  // The producer sets up the barriers and starts streaming without waiting
+  // for the consumers (a CTA that starts next to busy ones gets few issue
+  // slots; the first TMA copies should not queue behind its whole prologue).
   if (tid >= C::NCT) {  // ---------------- producer warp
+    if (tid == C::NCT) {
+      for (int s = 0; s < C::STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], C::NCW);
+      }
+      mbar_init(cbar, 1);
+      mbar_init(segdone, 1);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    named_arrive(2, C::THREADS);
     if (tid == C::NCT) {
       int it = 0, epis = 0;
       bool after_epilogue = false;
@@ -102,6 +105,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
   }
 
   // ------------------------------------------------------------ consumers
+  named_sync(2, C::THREADS);  // the producer has initialised the barriers
   // acc[i][p] holds the column pair (2p, 2p+1) of register-tile row i; one
   // FFMA2 updates a pair with A's element broadcast, so the 64 multiply-adds
   // per inner step cost 32 issue slots.

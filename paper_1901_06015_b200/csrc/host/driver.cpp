@@ -255,19 +255,17 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   // grid's last wave would run mostly empty: whole-tile CTAs for all but the
   // last full wave, then one CTA per slot sharing the rest as k-block ranges
   // (common.cuh: make_sched); bitwise identical to the classic grid.
-  // Thresholds measured on B200 (cfg2 sizes): with two CTAs per SM (DMMA)
-  // it wins up to a tail wave 80 % full (+2..7 %); with three per SM (FFMA,
-  // single-precision C) the older CTAs of an SM get most issue slots, the
-  // static ranges wait for the slowest one, and it only wins for an almost
-  // empty tail (< 10 %).  Inside a concurrent batch the classic grid stays:
-  // its hardware-scheduled tiles interleave with the other calls' kernels.
+  // Measured on B200 over the cfg2 sizes 1792..4096: +2..11 % for the DMMA
+  // and FFMA kernels whenever the tail wave is less than ~85 % full, neutral
+  // above.  Inside a concurrent batch the classic grid stays: its
+  // hardware-scheduled tiles interleave with the other calls' kernels.
   const int64_t slots = static_cast<int64_t>(sms) * per_sm;
   int sk_grid = 0;
   if (!exact && splits == 1 && tiles > slots && tiles % slots != 0 && tile.bn == 128) {
     int mode = 0;  // tuning override MDGEMM_STREAMK: 0 auto, 1 force on, -1 off
     if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
     const double tail = static_cast<double>(tiles % slots) / static_cast<double>(slots);
-    const bool wins = tail < (per_sm >= 3 ? 0.10 : 0.80);
+    const bool wins = tail < 0.85;
     if (mode > 0 || (mode == 0 && !shared && wins)) sk_grid = static_cast<int>(slots);
   }
   const size_t acc_size = single ? sizeof(float) : sizeof(double);
