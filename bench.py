@@ -214,7 +214,7 @@ def run_b200(args):
                 ops[key] = (t, v)
                 if role == "a":
                     a_bufs.append(t)
-    calls = []
+    calls, call_info = [], []  # call_info: (case id, useful flops, computation precision) per call
     for lab, m, n, k, al, be in items:
         j0, nb = shard[(lab, m, n, k)]
         dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
@@ -224,6 +224,8 @@ def run_b200(args):
         vc = ops[("c", dc, (m, nb))][1].with_comp_prec(comp)
         if nb > 0:
             calls.append((al, va, vb, be, vc))
+            cid = M.CaseLabel.parse(lab).case_id()
+            call_info.append((cid, M.flops_of_case(cid, m, nb, k), lab[3]))
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step():
@@ -266,11 +268,26 @@ def run_b200(args):
     flush.fill_(1)
     torch.cuda.synchronize()
     M.profile_begin()
+    call_events = []
     for al, va, vb, be, vc in calls:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record(stream)
         M.gemm_async(al, va, vb, be, vc, cfg, stream)
+        ev[1].record(stream)
+        call_events.append(ev)
     torch.cuda.synchronize()
     kstats = M.profile_end()
     serial_ms = sum(v["ms"] for v in kstats.values())
+    # per mixed-datatype case (BASELINE's metric): whole calls (packs + gemm) in the serialized step
+    per_case, pk0 = {}, peaks()
+    for (cid, fl, comp), (e0, e1) in zip(call_info, call_events):
+        c = per_case.setdefault(M.CASE_NAMES[cid], {"calls": 0, "flops": 0.0, "ms": 0.0, "ideal_ms": 0.0})
+        c["calls"] += 1
+        c["flops"] += fl
+        c["ms"] += e0.elapsed_time(e1)
+        c["ideal_ms"] += fl / ((pk0["ffma_tflops"] if comp == "s" else pk0["dmma_tflops"]) * 1e9)
+    per_case = {name: {"calls": c["calls"], "GFLOPS": round(c["flops"] / c["ms"] / 1e6, 1),
+                       "frac_of_peak": round(c["ideal_ms"] / c["ms"], 3)} for name, c in per_case.items()}
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -387,6 +404,7 @@ def run_b200(args):
         "roofline": roof,
         "kernel_share": kernel_share,
         "kernels": kernels,
+        "per_case": per_case,
         "serialized_step_ms": serial_ms,
         "gpu_launches": launches,
         "clocks": clocks,
