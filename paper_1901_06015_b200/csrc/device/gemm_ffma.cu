@@ -31,8 +31,8 @@ struct FfmaCfg {
   static constexpr int STAGE_A = BK * BM, STAGE_B = BK * BN;  // floats
   static constexpr size_t RING_BYTES = size_t(STAGES) * (STAGE_A + STAGE_B) * sizeof(float);
   // epilogue: the staged accumulator tile (EPI_ESZ = bytes per real element
-  // of C's storage) plus C chunks of at least half the tile
-  static constexpr size_t EPI_BYTES = size_t(BM) * BN * EPI_ESZ * 3 / 2;
+  // of C's storage) plus a C chunk buffer of at least 16 columns
+  static constexpr size_t EPI_BYTES = size_t(BM) * BN * EPI_ESZ + size_t(BM) * EPI_ESZ * 16;
   static constexpr size_t REGION = RING_BYTES > EPI_BYTES ? RING_BYTES : EPI_BYTES;
   // full[STAGES], empty[STAGES], C-chunk barrier, segment-done barrier
   static constexpr size_t SMEM = REGION + (2 * STAGES + 2) * sizeof(uint64_t);
@@ -226,14 +226,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
 
 using Big = FfmaCfg<128, 128, 8, 1>;
 using Pair = FfmaCfg<64, 128, 8, 2>;  // two CTAs per SM: epilogues overlap mainloops
-// single-precision C: a 4-byte staging tile leaves room for three CTAs per SM
-using Pair3 = FfmaCfg<64, 128, 6, 3, 4>;
+// Three CTAs per SM (72 KB each): a 6-stage ring, and an epilogue that stages
+// the tile in C's storage precision with a C chunk buffer of >= 16 columns.
+using Pair3 = FfmaCfg<64, 128, 6, 3, 4>;   // single-precision C
+using Pair3d = FfmaCfg<64, 128, 6, 3, 8>;  // double-precision C
 using Small = FfmaCfg<64, 64, 6, 4>;
 
 // The configuration a tile shape runs with for C's storage datatype.
 template <class C, int CDT>
-using CfgFor = typename std::conditional<(C::BM == 64 && C::BN == 128 && (CDT == MDG_DT_S || CDT == MDG_DT_C)),
-                                         Pair3, C>::type;
+using CfgFor = typename std::conditional<
+    (C::BM == 64 && C::BN == 128),
+    typename std::conditional<(CDT == MDG_DT_S || CDT == MDG_DT_C), Pair3, Pair3d>::type, C>::type;
 
 template <class C>
 cudaError_t run(const GemmDesc& d, cudaStream_t s) {

@@ -264,9 +264,24 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   if (!exact && splits == 1 && tiles > slots && tiles % slots != 0 && tile.bn == 128) {
     int mode = 0;  // tuning override MDGEMM_STREAMK: 0 auto, 1 force on, -1 off
     if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
+    // Only where the tail matters (few waves) and tiles are mainloop-bound:
+    // with a short k the epilogue dominates and the stream-K variant's
+    // heavier epilogue costs more than the tail (cfg5 k=64: -43 %).
     const double tail = static_cast<double>(tiles % slots) / static_cast<double>(slots);
-    const bool wins = tail < 0.85;
-    if (mode > 0 || (mode == 0 && !shared && wins)) sk_grid = static_cast<int>(slots);
+    const bool wins = tail < 0.85 && tiles < 16 * slots && nk >= 32;
+    if (mode == 1 || (mode == 0 && !shared && wins)) sk_grid = static_cast<int>(slots);
+  }
+  // The segment-loop kernel with one whole tile per CTA (sk_grid = tiles:
+  // make_sched gives every CTA its own tile) is the classic schedule.  ptxas
+  // compiles the FFMA 128x128 mainloop 4-6 % faster in that variant
+  // (measured, cfg4: 61.2 -> 64.0 TFLOP/s), so it always runs there;
+  // MDGEMM_STREAMK=2 forces it for every tile shape (experiments).
+  {
+    const char* f = std::getenv("MDGEMM_STREAMK");
+    const bool force = f && std::atoi(f) == 2;
+    if (!exact && splits == 1 && sk_grid == 0 && tiles > 0 &&
+        ((single && tile.bm == 128 && tile.bn == 128) || (force && tile.bn == 128)))
+      sk_grid = static_cast<int>(tiles);
   }
   const size_t acc_size = single ? sizeof(float) : sizeof(double);
   const size_t off_b = (pa.bytes + 255) / 256 * 256;
