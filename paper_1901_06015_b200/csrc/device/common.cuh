@@ -279,6 +279,21 @@ __device__ __forceinline__ void trace_stamp(unsigned long long* trace, unsigned 
   r[4] = globaltimer();
 }
 
+// 2-D TMA tensor copies of one box (coordinates in elements of the map).
+__device__ __forceinline__ void tensor_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+
 // Warm L2 with a global range ahead of the TMA ring (no shared memory, no
 // completion): hides DRAM latency that a STAGES-deep ring cannot.
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
@@ -327,6 +342,30 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 // `emit(put)` must call put(r, c, value) for every accumulator the calling
 // thread holds.  Code size matters: this runs once per tile after a long
 // mainloop, so it stays a compact rolled loop.
+// Short inner dimension: the producer warms L2 with the C tile the epilogue
+// will read (same geometry as fast_epilogue's TMA path), so the epilogue's C
+// chunk loads hit L2 instead of waiting on DRAM.
+template <int CDT>
+__device__ __forceinline__ void prefetch_c_tile(const DEpilogue& e, int64_t r0, int64_t c0, int BM, int BN) {
+  using O = OutType<CDT>;
+  using R = typename O::R;
+  if (e.beta.is_zero) return;
+  const bool prow = e.pair == MDG_PAIR_ROWS, pcol = e.pair == MDG_PAIR_COLS;
+  const int orows = prow ? BM / 2 : BM, ocols = pcol ? BN / 2 : BN;
+  const int64_t oi0 = prow ? r0 / 2 : r0, oj0 = pcol ? c0 / 2 : c0;
+  const int64_t om = prow ? e.me / 2 : e.me, on = pcol ? e.ne / 2 : e.ne;
+  if (e.out.rs != 1 || oi0 >= om || oj0 >= on) return;
+  const int rows = static_cast<int>(om - oi0 < orows ? om - oi0 : orows);
+  const int cols = static_cast<int>(on - oj0 < ocols ? on - oj0 : ocols);
+  const uint32_t bytes = static_cast<uint32_t>(rows * O::ESZ) & ~15u;
+  if (bytes == 0) return;
+  const R* out = reinterpret_cast<const R*>(e.out.base);
+  for (int j = 0; j < cols; ++j) {
+    const R* p = out + (oi0 + (oj0 + j) * e.out.cs) * O::NC;
+    if ((reinterpret_cast<uint64_t>(p) & 15) == 0) bulk_prefetch_l2(p, bytes);
+  }
+}
+
 template <int CDT, class Emit>
 __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t region, uint64_t* cbar,
                                               const DEpilogue& e, int64_t r0, int64_t c0, int BM, int BN, int tid,
@@ -343,18 +382,22 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
   const bool conj = e.out.conj != 0;
   const uint32_t col_bytes = orows * O::ESZ;
   R* const out = reinterpret_cast<R*>(e.out.base);
-  const uint64_t first = reinterpret_cast<uint64_t>(out + (oi0 * e.out.rs + oj0 * e.out.cs) * NC);
-  const bool tma = e.out.rs == 1 && oi0 + orows <= om && oj0 + ocols <= on && (first & 15) == 0 &&
-                   (col_bytes & 15) == 0 && ((e.out.cs * O::ESZ) & 15) == 0;
   unsigned char* tbuf = smem;
   unsigned char* cbuf = smem + ocols * col_bytes;
-  const int CH = tma ? min(ocols, static_cast<int>((region - ocols * col_bytes) / col_bytes)) : ocols;
+  // TMA path: C moves as 2-D tensor boxes of C_BOX_COLS columns (loads into
+  // cbuf, results written back into tbuf and stored from there); the tensor
+  // map clips edge tiles.  Chunks are whole boxes that fit beside the tile.
+  const int CH_FIT = static_cast<int>((region - ocols * col_bytes) / col_bytes) / C_BOX_COLS * C_BOX_COLS;
+  const bool tma = e.cmap_ok != 0 && CH_FIT >= C_BOX_COLS;
+  const int CH = tma ? min(ocols, CH_FIT) : ocols;
+  const CUtensorMap* map = &e.cmap;
+  const int x0 = static_cast<int>(oi0 * NC);
   auto load_chunk = [&](int j0) {
-    const int ch = min(CH, ocols - j0);
+    const int nb = (min(CH, ocols - j0) + C_BOX_COLS - 1) / C_BOX_COLS;
     fence_proxy_async();
-    mbar_arrive_expect_tx(cbar, ch * col_bytes);
-    for (int j = 0; j < ch; ++j)
-      bulk_g2s(cbuf + j * col_bytes, out + (oi0 + (oj0 + j0 + j) * e.out.cs) * NC, col_bytes, cbar);
+    mbar_arrive_expect_tx(cbar, nb * C_BOX_COLS * col_bytes);
+    for (int b = 0; b < nb; ++b)
+      tensor_load_2d(cbuf + b * C_BOX_COLS * col_bytes, map, x0, static_cast<int>(oj0 + j0 + b * C_BOX_COLS), cbar);
   };
   if (tma && reads_c && tid == 0) load_chunk(0);
   emit([&](int r, int c, double v) {
@@ -374,21 +417,24 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
       const int nv = ch * orows / VEC;
       for (int v = tid; v < nv; v += nthr) {
         const int idx = v * VEC;  // element within the chunk, column-major
-        const int oi = idx % orows, oj = idx / orows;
         union {
           uint4 u;
           R x[VEC * NC];
         } cv, tv;
-        tv.u = *reinterpret_cast<const uint4*>(tbuf + (static_cast<size_t>(j0) * orows + idx) * O::ESZ);
+        uint4* tp = reinterpret_cast<uint4*>(tbuf + (static_cast<size_t>(j0) * orows + idx) * O::ESZ);
+        tv.u = *tp;
         cv.u = reads_c ? *reinterpret_cast<const uint4*>(cbuf + static_cast<size_t>(idx) * O::ESZ) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < VEC; ++u) combine_typed<CDT>(e.beta, conj, &cv.x[u * NC], &tv.x[u * NC]);
-        *reinterpret_cast<uint4*>(out + (oi0 + oi + (oj0 + j0 + oj) * e.out.cs) * NC) = cv.u;
+        *tp = cv.u;
       }
-      if (j0 + ch < ocols) {  // another chunk will land in cbuf: order these reads before it
-        fence_proxy_async();
-        named_sync(1, nthr);
-        if (reads_c && tid == 0) load_chunk(j0 + ch);
+      fence_proxy_async();  // generic writes of tbuf before the async-proxy store reads them
+      named_sync(1, nthr);  // ... and every thread is done with cbuf
+      if (tid == 0) {
+        for (int b = 0; b < ch; b += C_BOX_COLS)
+          tensor_store_2d(map, x0, static_cast<int>(oj0 + j0 + b), tbuf + static_cast<size_t>(j0 + b) * col_bytes);
+        bulk_commit();
+        if (reads_c && j0 + ch < ocols) load_chunk(j0 + ch);
       }
     } else {
       const int n = ch * orows;
@@ -407,6 +453,7 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
       }
     }
   }
+  if (tma && tid == 0) bulk_wait_read();  // the stores have read tbuf: the smem may be reused / released
 }
 
 // Grouped tile raster: walks `group` tile-rows at a time.  A short group

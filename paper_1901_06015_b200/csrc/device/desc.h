@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched at run time)
 #include <cuda_runtime.h>
 
 #include "mdgemm_b200.h"
@@ -29,12 +30,17 @@ struct DBeta {
 // computation maps onto `out` directly (pair NONE), or pairs rows (2i,2i+1)
 // / columns (2j,2j+1) into one complex element.
 struct DEpilogue {
+  // C as a 2-D tiled tensor (inner dimension: rows x components in C's real
+  // type, outer: columns) for TMA tensor loads/stores of C_BOX_COLS-column
+  // boxes; valid when cmap_ok (column-major C with 16-byte aligned columns).
+  CUtensorMap cmap;
   DView out;
   int32_t pair;
-  int32_t reserved;
+  int32_t cmap_ok;
   DBeta beta;
   int64_t me, ne;
 };
+constexpr int C_BOX_COLS = 16;
 
 // Panel geometry of one packed operand, in real elements of the computation
 // precision: panels of `pd` rows (left) / columns (right), `lpad` inner-
@@ -88,6 +94,8 @@ struct GemmDesc {
   unsigned long long* trace;  // tuning only (MDGEMM_TRACE): TRACE_WORDS stamps per CTA
   void* sk_partials;   // stream-K: sk_grid partial tiles in thread-fragment order, comp precision
   int* sk_flags;       // stream-K: sk_grid publish flags, zeroed before the launch
+  int32_t c_prefetch;  // producer warms L2 with the C tile after its loads (short k)
+  int32_t pad0;
 };
 
 // Stream-K hybrid grid (common.cuh: make_sched): dp whole-tile CTAs, then G

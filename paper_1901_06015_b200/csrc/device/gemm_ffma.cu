@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
                    &full[s]);
         }
         after_epilogue = sg.kind == SEG_FULL || sg.kind == SEG_END;
+        if (d.c_prefetch && after_epilogue)
+          prefetch_c_tile<CDT>(d.epi, static_cast<int64_t>(tm) * C::BM, static_cast<int64_t>(tn) * C::BN, C::BM, C::BN);
       }
     }
     return;

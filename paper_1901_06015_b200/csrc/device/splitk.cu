@@ -13,7 +13,8 @@ namespace {
 constexpr int RED_THREADS = 256;
 
 template <int CDT, typename AccT>
-__global__ void __launch_bounds__(RED_THREADS) splitk_reduce_kernel(GemmDesc d, int BM, int BN, uint32_t region) {
+__global__ void __launch_bounds__(RED_THREADS)
+    splitk_reduce_kernel(const __grid_constant__ GemmDesc d, int BM, int BN, uint32_t region) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + region);
   if (threadIdx.x == 0) {

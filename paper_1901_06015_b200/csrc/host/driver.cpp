@@ -185,6 +185,40 @@ std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Da
   return pack_geometry(src, side, format, target, reg_block, 0).bytes;
 }
 
+// C as a 2-D TMA tensor for the fused epilogue (common.cuh: fast_epilogue):
+// inner dimension = rows x components in C's real type, outer = columns,
+// boxes of (tile rows) x C_BOX_COLS.  Column-major C with 16-byte aligned
+// columns only; anything else keeps the element-wise epilogue path.
+static bool encode_c_map(mdg::DEpilogue& e, int bm) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<Encode>(nullptr);
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode) return false;
+  const bool single = e.out.dtype == MDG_DT_S || e.out.dtype == MDG_DT_C;
+  const int nc = (e.out.dtype == MDG_DT_C || e.out.dtype == MDG_DT_Z) ? 2 : 1;
+  const int esz = (single ? 4 : 8) * nc;
+  const int orows = e.pair == MDG_PAIR_ROWS ? bm / 2 : bm;
+  const auto base = reinterpret_cast<uintptr_t>(e.out.base);
+  if (e.out.rs != 1 || e.out.m <= 0 || e.out.n <= 0 || base % 16 || (e.out.cs * esz) % 16 || (orows * esz) % 16 ||
+      orows * nc > 256)
+    return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(e.out.m * nc), static_cast<cuuint64_t>(e.out.n)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.out.cs * esz)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(orows * nc), static_cast<cuuint32_t>(mdg::C_BOX_COLS)};
+  const cuuint32_t estride[2] = {1, 1};
+  return encode(&e.cmap, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                e.out.base, dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Resident CTAs per SM of a fast kernel (occupancy query, cached per
 // tile shape x kernel x C datatype; the value is the same on every B200).
 static int ctas_per_sm(const mdg::FastTile& t, bool single, int cdt) {
@@ -315,6 +349,9 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   g.epi.beta = to_dbeta(p.beta);
   g.epi.me = p.m;
   g.epi.ne = p.n;
+  g.epi.cmap_ok = !exact && encode_c_map(g.epi, tile.bm) ? 1 : 0;
+  if (const char* f = std::getenv("MDGEMM_C_TMA"))  // tuning: 0 = element-wise epilogue
+    if (std::atoi(f) == 0) g.epi.cmap_ok = 0;
   g.kc = p.params.kc;
   g.seed_beta = p.beta.re;
   // Short inner dimension: C traffic dominates, walk whole tile-columns so the
@@ -329,6 +366,8 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   g.sk_partials = sk_grid > 0 ? wsa + off_p : nullptr;
   g.sk_flags = sk_grid > 0 ? reinterpret_cast<int*>(wsa + off_f) : nullptr;
   g.prefetch = 0;
+  g.c_prefetch = nk <= 16 ? 1 : 0;  // short k: the epilogue's C traffic is the critical path
+  if (const char* force = std::getenv("MDGEMM_C_PREFETCH")) g.c_prefetch = std::atoi(force);
   if (const char* force = std::getenv("MDGEMM_PREFETCH")) g.prefetch = std::atoi(force);
 
   if (err == cudaSuccess) {
