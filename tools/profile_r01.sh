@@ -1,17 +1,21 @@
 #!/bin/bash
 # Round-1 profiling on one B200: launch list of a short bench run, then one
-# `ncu --set full` capture per gemm kernel family (each only after the same
-# command exited 0 without ncu).
+# `ncu --set full` capture per kernel family (each only after the same
+# command exited 0 without ncu), exported to CSV for profiles/r01/.
 set -u
-mkdir -p gpurun_out
+mkdir -p gpurun_out/prof
+O=gpurun_out/prof
 CMD="python bench.py --labels dddd,zzzd,ssss,cccs,dssd,sddd --size 4096 --steps 1 --warmup 1 --no-e2e --no-cpu"
-$CMD > gpurun_out/prof_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
+$CMD > $O/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1
 echo launches_rc=$?
-$CMD > gpurun_out/prof_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:gemm_dmma -s 1 -c 1 -o gpurun_out/prof_dmma -f $CMD > gpurun_out/ncu_dmma.log 2>&1
-echo dmma_rc=$?
-ncu --set full --clock-control none --import-source on -k regex:gemm_ffma -s 1 -c 1 -o gpurun_out/prof_ffma -f $CMD > gpurun_out/ncu_ffma.log 2>&1
-echo ffma_rc=$?
-ncu --set full --clock-control none --import-source on -k regex:pack_kernel -s 4 -c 2 -o gpurun_out/prof_pack -f $CMD > gpurun_out/ncu_pack.log 2>&1
-echo pack_rc=$?
+# one kernel each: zzzd (DMMA, 1m: me=8192 ne=4096 ke=8192), cccs (FFMA, same dims), a 1e pack
+for spec in "dmma gemm_dmma zzzd" "ffma gemm_ffma cccs" "pack pack_kernel zzzd"; do
+  set -- $spec
+  C1="python bench.py --labels $3 --size 4096 --steps 1 --warmup 1 --no-e2e --no-cpu"
+  $C1 > $O/plain_$1.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$2 -s 2 -c 1 -o $O/prof_$1 -f $C1 > $O/ncu_$1.log 2>&1
+  echo $1_rc=$?
+  ncu -i $O/prof_$1.ncu-rep --page raw --csv > $O/ncu_$1_raw.csv 2>/dev/null
+  ncu -i $O/prof_$1.ncu-rep --page details --csv > $O/ncu_$1_details.csv 2>/dev/null
+done
