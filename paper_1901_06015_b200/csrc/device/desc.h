@@ -126,6 +126,10 @@ FastTile choose_dmma_tile(int64_t me, int64_t ne, int sms);
 FastTile choose_ffma_tile(int64_t me, int64_t ne, int sms);
 cudaError_t launch_gemm_dmma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
 cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t s);
+// Warp-specialised persistent DMMA kernel (gemm_dmma_ws.cu): 128x128 tiles,
+// `grid` CTAs (one per SM); d.sk_grid = grid turns on the stream-K tail.
+size_t dmma_ws_smem(int cdt);
+cudaError_t launch_gemm_dmma_ws(const GemmDesc& d, int grid, cudaStream_t s);
 // Resident CTAs per SM of the kernel a tile shape / C datatype launches
 // (occupancy query; sizes the split-K and stream-K grids).
 int dmma_ctas_per_sm(const FastTile& t, int cdt);

@@ -1,0 +1,360 @@
+// FAST numerics, computation precision double: warp-specialised persistent
+// variant of the DMMA kernel (gemm_dmma.cu), one CTA per SM.
+//
+//   warps 0-7  MMA: one 128x128 tile cooperatively (64x32 warp tiles of
+//              DMMA.8x8x4), two warps per SM sub-partition (one warp per
+//              sub-partition reaches only ~65 % of the DMMA rate, measured
+//              by `tools/peaks 10 occ`);
+//   warp  8    producer: one lane streams 16-deep A/B slabs with TMA bulk
+//              copies into a STAGES-deep ring;
+//   warp  9    C mover: one lane moves C through a tile-sized buffer in C's
+//              storage precision with 2-D TMA tensor copies -- it loads the
+//              NEXT tile's C while the MMA warps run that tile's mainloop,
+//              and stores each finished tile.
+//
+// After its mainloop the MMA warps combine their accumulators with the C
+// tile already in shared memory (accumulate_element, kernels.cpp:79-95, via
+// combine_typed -- the same arithmetic as the classic epilogue) and write the
+// result in place; the C mover stores it and immediately loads the next C.
+// So the C traffic of a tile overlaps the next tile's mainloop, and the MMA
+// warps' epilogue is a pass over shared memory.  mbarriers: c_full (C tile
+// landed, or nothing to load when beta = 0) and res_full (results written).
+//
+// Each CTA walks tiles blockIdx + w * gridDim (wave-major, so concurrently
+// running CTAs share panels in L2); with d.sk_grid the partial last wave is
+// shared as stream-K ranges whose split tiles are finished by SEEDING the
+// next CTA's accumulators (common.cuh), so every element's rounding sequence
+// -- and the result, bitwise -- is the classic kernel's.  One CTA per SM
+// also means no co-resident CTA competes for issue slots: CTAs progress in
+// step and the static schedule stays balanced.  Requires a column-major,
+// 16-byte aligned C (a TMA tensor map, d.epi.cmap_ok); the driver keeps the
+// classic kernel otherwise.
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace mdg {
+namespace {
+
+constexpr int WS_BM = 128, WS_BN = 128, WS_BK = 16;
+constexpr int WS_WM = 2, WS_WN = 4;  // 8 MMA warps, 64x32 warp tiles
+constexpr int WS_MMA_WARPS = WS_WM * WS_WN;
+constexpr int WS_MMA_THREADS = WS_MMA_WARPS * 32;
+constexpr int WS_PROD_WARP = WS_MMA_WARPS;
+constexpr int WS_CMOV_WARP = WS_MMA_WARPS + 1;
+constexpr int WS_THREADS = (WS_MMA_WARPS + 2) * 32;
+constexpr int WS_MT = 8, WS_NT = 4;
+constexpr int WS_STAGE_A = WS_BK * WS_BM, WS_STAGE_B = WS_BK * WS_BN;  // doubles
+
+template <int CDT>
+struct WsCfg {
+  using O = OutType<CDT>;
+  static constexpr int ESZR = O::kSingle ? 4 : 8;                   // bytes per real element of C
+  static constexpr size_t CTILE = size_t(WS_BM) * WS_BN * ESZR;     // 64 / 128 KB
+  static constexpr int STAGES = O::kSingle ? 4 : 3;                 // 128 / 96 KB ring
+  static constexpr size_t RING = size_t(STAGES) * (WS_STAGE_A + WS_STAGE_B) * sizeof(double);
+  static constexpr size_t SMEM = RING + CTILE + (2 * STAGES + 2) * sizeof(uint64_t);
+};
+
+// Persistent schedule of CTA b out of G: whole tiles b + w G (w < dpw), then
+// (stream-K) the CTA's k-block range of the last G + tiles % G tiles.
+struct WsSched {
+  int nk, nseg, dpw, G;
+  int start_tile, start_k1;  // SEG_START (start_k1 == 0: none)
+  int full0, full1;          // whole tiles of the range
+  int end_tile, end_k0;      // SEG_END (end_k0 == 0: none)
+};
+
+__device__ __forceinline__ WsSched ws_sched(int64_t tiles, int nk, bool sk) {
+  WsSched s{};
+  s.nk = nk;
+  s.G = static_cast<int>(gridDim.x);
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t R = tiles % G;
+  if (!sk || R == 0) {
+    s.dpw = static_cast<int>((tiles - b + G - 1) / G);
+    s.nseg = s.dpw;
+    return s;
+  }
+  const int64_t dp = (tiles / G - 1) * G;
+  s.dpw = static_cast<int>(dp / G);
+  const int64_t U = (tiles - dp) * nk;
+  const int64_t u0 = dp * nk + b * U / G, u1 = dp * nk + (b + 1) * U / G;
+  s.start_tile = static_cast<int>(u1 / nk);
+  s.start_k1 = static_cast<int>(u1 % nk);
+  s.end_tile = static_cast<int>(u0 / nk);
+  s.end_k0 = static_cast<int>(u0 % nk);
+  s.full0 = static_cast<int>((u0 + nk - 1) / nk);
+  s.full1 = s.start_tile;
+  s.nseg = (s.start_k1 != 0) + s.dpw + (s.full1 - s.full0) + (s.end_k0 != 0);
+  return s;
+}
+
+// Order: SEG_START first (the next CTA's SEG_END waits for it), whole tiles,
+// the range's whole tiles, SEG_END last.
+__device__ __forceinline__ Seg ws_seg(const WsSched& s, int idx) {
+  if (s.start_k1 != 0) {
+    if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
+    --idx;
+  }
+  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
+  idx -= s.dpw;
+  if (idx < s.full1 - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
+  return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
+}
+
+__device__ __forceinline__ void dmma884_ws(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int CDT>
+__global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __grid_constant__ GemmDesc d) {
+  using W = WsCfg<CDT>;
+  using O = OutType<CDT>;
+  using R = typename O::R;
+  constexpr int NC = O::NC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = sA + W::STAGES * WS_STAGE_A;
+  unsigned char* ctile = smem + W::RING;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctile + W::CTILE);
+  uint64_t* empty = full + W::STAGES;
+  uint64_t* c_full = empty + W::STAGES;  // C mover -> MMA warps: this tile's C is in ctile
+  uint64_t* res_full = c_full + 1;       // MMA warps -> C mover: results written (one arrive per warp)
+
+  const int tiles_m = static_cast<int>((d.me + WS_BM - 1) / WS_BM);
+  const int tiles_n = static_cast<int>((d.ne + WS_BN - 1) / WS_BN);
+  const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
+  const int64_t lpad = d.a.lpad;
+  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0);
+
+  const DEpilogue& e = d.epi;
+  const bool prow = e.pair == MDG_PAIR_ROWS, pcol = e.pair == MDG_PAIR_COLS;
+  const int orows = prow ? WS_BM / 2 : WS_BM, ocols = pcol ? WS_BN / 2 : WS_BN;
+  const bool reads_c = !e.beta.is_zero;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == WS_PROD_WARP) {  // ------------------------------------------ producer
+    if (lane == 0) {
+      for (int s = 0; s < W::STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], WS_MMA_WARPS);
+      }
+      mbar_init(c_full, 1);
+      mbar_init(res_full, WS_MMA_WARPS);
+      mbar_fence_init();
+    }
+    __syncwarp();
+    named_arrive(2, WS_THREADS);
+    if (lane != 0) return;
+    int it = 0;
+    for (int si = 0; si < sc.nseg; ++si) {
+      const Seg sg = ws_seg(sc, si);
+      int tm, tn;
+      tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+      const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * WS_BM * lpad;
+      const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * WS_BN * lpad;
+      for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+        const int s = it % W::STAGES;
+        if (it >= W::STAGES) mbar_wait(&empty[s], ((it / W::STAGES) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], (WS_STAGE_A + WS_STAGE_B) * sizeof(double));
+        bulk_g2s(sA + s * WS_STAGE_A, Ag + static_cast<int64_t>(kb) * WS_STAGE_A, WS_STAGE_A * sizeof(double),
+                 &full[s]);
+        bulk_g2s(sB + s * WS_STAGE_B, Bg + static_cast<int64_t>(kb) * WS_STAGE_B, WS_STAGE_B * sizeof(double),
+                 &full[s]);
+      }
+    }
+    return;
+  }
+  named_sync(2, WS_THREADS);  // barriers initialised
+
+  if (warp == WS_CMOV_WARP) {  // ------------------------------------------ C mover
+    if (lane != 0) return;
+    const uint32_t col_bytes = orows * O::ESZ;
+    const uint32_t tile_bytes = static_cast<uint32_t>(ocols) * col_bytes;
+    auto coords = [&](const Seg& sg, int& x0, int& y0) {
+      int tm, tn;
+      tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+      x0 = (prow ? tm * (WS_BM / 2) : tm * WS_BM) * NC;
+      y0 = pcol ? tn * (WS_BN / 2) : tn * WS_BN;
+    };
+    auto load = [&](const Seg& sg) {  // C of the tile the MMA warps finish next
+      if (!reads_c) {
+        mbar_arrive(c_full);
+        return;
+      }
+      int x0, y0;
+      coords(sg, x0, y0);
+      mbar_arrive_expect_tx(c_full, tile_bytes);
+      for (int b = 0; b < ocols; b += C_BOX_COLS)
+        tensor_load_2d(ctile + static_cast<size_t>(b) * col_bytes, &e.cmap, x0, y0 + b, c_full);
+    };
+    int epis = 0, pending = -1;  // pending: segment whose C is loaded and whose results are awaited
+    for (int si = 0; si < sc.nseg; ++si) {
+      const Seg sg = ws_seg(sc, si);
+      if (sg.kind == SEG_START) continue;
+      if (pending >= 0) {  // store the previous tile, then reuse the buffer for this one
+        mbar_wait(res_full, epis & 1);
+        int x0, y0;
+        coords(ws_seg(sc, pending), x0, y0);
+        for (int b = 0; b < ocols; b += C_BOX_COLS)
+          tensor_store_2d(&e.cmap, x0, y0 + b, ctile + static_cast<size_t>(b) * col_bytes);
+        bulk_commit();
+        bulk_wait_read();
+        ++epis;
+      }
+      fence_proxy_async();
+      load(sg);
+      pending = si;
+    }
+    if (pending >= 0) {
+      mbar_wait(res_full, epis & 1);
+      int x0, y0;
+      coords(ws_seg(sc, pending), x0, y0);
+      for (int b = 0; b < ocols; b += C_BOX_COLS)
+        tensor_store_2d(&e.cmap, x0, y0 + b, ctile + static_cast<size_t>(b) * col_bytes);
+      bulk_commit();
+      bulk_wait_read();  // the smem must outlive the store's reads
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- MMA warps
+  const int tid = threadIdx.x;
+  const int wm = warp % WS_WM, wn = warp / WS_WM;
+  const int g = lane >> 2, tig = lane & 3;
+  const bool conj = e.out.conj != 0;
+  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+  const double* a_base = sA + wm * 64 + g + tig * WS_BM;
+  const double* b_base = sB + wn * 32 + g + tig * WS_BN;
+  R* const ct = reinterpret_cast<R*>(ctile);
+  int it = 0, epis = 0;
+  for (int si = 0; si < sc.nseg; ++si) {
+    const Seg sg = ws_seg(sc, si);
+    double acc[WS_MT][WS_NT][2];
+    if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      if (tid == 0) flag_acquire_wait(d.sk_flags + blockIdx.x - 1);
+      named_sync(1, WS_MMA_THREADS);
+      const double* slot =
+          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x - 1) * (WS_BM * WS_BN);
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            acc[i][j][h] = __ldcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid);
+    } else {
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+      const int s = it % W::STAGES;
+      mbar_wait_u32(full_u + 8 * s, (it / W::STAGES) & 1);
+      const double* a = a_base + s * WS_STAGE_A;
+      const double* b = b_base + s * WS_STAGE_B;
+#pragma unroll
+      for (int kk = 0; kk < WS_BK; kk += 4) {
+        double af[WS_MT], bf[WS_NT];
+#pragma unroll
+        for (int i = 0; i < WS_MT; ++i) af[i] = a[kk * WS_BM + i * 8];
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j) bf[j] = b[kk * WS_BN + j * 8];
+#pragma unroll
+        for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+          for (int j = 0; j < WS_NT; ++j) dmma884_ws(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      fence_proxy_async();  // generic reads of the stage before its TMA refill
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
+    }
+    if (sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
+      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x) * (WS_BM * WS_BN);
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
+      __threadfence();
+      named_sync(1, WS_MMA_THREADS);
+      if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
+      continue;
+    }
+    // combine with this tile's C (already in ctile) in place
+    mbar_wait(c_full, epis & 1);
+#pragma unroll
+    for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+      for (int j = 0; j < WS_NT; ++j) {
+        const int r = wm * 64 + i * 8 + g, c = wn * 32 + j * 8 + 2 * tig;
+        const double a0 = acc[i][j][0], a1 = acc[i][j][1];  // (r, c), (r, c + 1)
+        if constexpr (NC == 1) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            R* p = ct + (c + h) * orows + r;
+            R cv = reads_c ? *p : R(0);
+            const R tv = static_cast<R>(h ? a1 : a0);
+            combine_typed<CDT>(e.beta, conj, &cv, &tv);
+            *p = cv;
+          }
+        } else {
+          // complex C: a column pair (pcol: re, im of element (r, c/2)) or a
+          // row pair held by lanes g and g^1 (prow: element (r/2, c) for even
+          // g, (r/2, c+1) for odd g after one exchange)
+          R tv[2];
+          R* p;
+          if (pcol) {
+            tv[0] = static_cast<R>(a0);
+            tv[1] = static_cast<R>(a1);
+            p = ct + ((c >> 1) * orows + r) * 2;
+          } else {
+            const double other = __shfl_xor_sync(0xffffffffu, (g & 1) ? a0 : a1, 4);
+            const bool odd = g & 1;
+            tv[0] = static_cast<R>(odd ? other : a0);
+            tv[1] = static_cast<R>(odd ? a1 : other);
+            p = ct + ((odd ? c + 1 : c) * orows + (r >> 1)) * 2;
+          }
+          R cv[2] = {R(0), R(0)};
+          if (reads_c) {
+            cv[0] = p[0];
+            cv[1] = p[1];
+          }
+          combine_typed<CDT>(e.beta, conj, cv, tv);
+          p[0] = cv[0];
+          p[1] = cv[1];
+        }
+      }
+    fence_proxy_async();  // generic writes of ctile before the C mover's TMA store reads them
+    __syncwarp();
+    if (lane == 0) mbar_arrive(res_full);
+    ++epis;
+  }
+}
+
+}  // namespace
+
+size_t dmma_ws_smem(int cdt) {
+  size_t s = 0;
+  MDG_DISPATCH_CDT(cdt, CDT, { s = WsCfg<CDT>::SMEM; });
+  return s;
+}
+
+cudaError_t launch_gemm_dmma_ws(const GemmDesc& d, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
+    auto kern = gemm_dmma_ws_kernel<CDT>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(WsCfg<CDT>::SMEM));
+    if (e != cudaSuccess) return e;
+    kern<<<static_cast<unsigned>(grid), WS_THREADS, WsCfg<CDT>::SMEM, s>>>(d);
+  });
+  return cudaGetLastError();
+}
+
+}  // namespace mdg

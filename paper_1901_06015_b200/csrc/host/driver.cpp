@@ -270,6 +270,28 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
 
   mdg::FastTile tile{64, 64, 1};
   if (!exact) tile = single ? mdg::choose_ffma_tile(p.m, p.n, sms) : mdg::choose_dmma_tile(p.m, p.n, sms);
+  // Warp-specialised persistent DMMA kernel (gemm_dmma_ws.cu): 128x128 tiles,
+  // one CTA per SM, the epilogue of one tile under the next tile's mainloop.
+  bool dmma_ws = false;
+  if (!exact && !single) {
+    int mode = 0;  // MDGEMM_DMMA_WS: 1 force on (where it applies), -1 off, 0 auto
+    if (const char* f = std::getenv("MDGEMM_DMMA_WS")) mode = std::atoi(f);
+    const int64_t t128 = ((p.m + 127) / 128) * ((p.n + 127) / 128);
+    mdg::DEpilogue probe{};  // the kernel moves C only through a TMA tensor map
+    probe.out = to_dview(p.c);
+    probe.pair = static_cast<int32_t>(p.pair_axis);
+    const bool complex_c = probe.out.dtype == MDG_DT_C || probe.out.dtype == MDG_DT_Z;
+    const bool c_ok = encode_c_map(probe, 128) && (!complex_c || probe.pair != MDG_PAIR_NONE);
+    // auto: real C (measured +1..7 % over the classic kernel at the cfg2
+    // sizes 2048-4096; complex C -1..2 %), one full wave of 128x128 tiles,
+    // and the GPU to itself (a persistent grid inside a concurrent batch
+    // would wait for slots the other calls hold; MDGEMM_DMMA_WS=2 allows it)
+    const bool want = mode == 1 || (mode == 0 && !complex_c && !shared) || (mode == 2 && !complex_c);
+    if (want && t128 >= sms && c_ok) {
+      dmma_ws = true;
+      tile = mdg::FastTile{128, 128, 16};
+    }
+  }
   const int64_t lpad = (p.k + tile.bk - 1) / tile.bk * tile.bk;
 
   Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, tile.bm, lpad);
@@ -278,9 +300,9 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   // Split-K when the tile grid cannot fill the machine (deterministic: the
   // partial tiles are summed in split order by the reduce pass).
   const int64_t tiles = ((p.m + tile.bm - 1) / tile.bm) * ((p.n + tile.bn - 1) / tile.bn);
-  const int per_sm = exact ? 1 : ctas_per_sm(tile, single, to_dview(p.c).dtype);
+  const int per_sm = exact || dmma_ws ? 1 : ctas_per_sm(tile, single, to_dview(p.c).dtype);
   const int64_t nk = lpad / tile.bk;
-  int splits = exact ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
+  int splits = exact || dmma_ws ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
   int kb_per_split = static_cast<int>(nk);
   if (splits > 1) {
     kb_per_split = static_cast<int>((nk + splits - 1) / splits);
@@ -296,7 +318,14 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   // hardware-scheduled tiles interleave with the other calls' kernels.
   const int64_t slots = static_cast<int64_t>(sms) * per_sm;
   int sk_grid = 0;
-  if (!exact && splits == 1 && tiles > slots && tiles % slots != 0 && tile.bn == 128) {
+  int ws_grid = 0;  // persistent grid of the warp-specialised kernel
+  if (dmma_ws) {
+    ws_grid = static_cast<int>(std::min<int64_t>(tiles, sms));
+    int mode = 0;
+    if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
+    // stream-K tail: CTAs of this kernel progress in step (one per SM)
+    if (mode >= 0 && tiles > sms && tiles % sms != 0 && nk >= 8) sk_grid = sms;
+  } else if (!exact && splits == 1 && tiles > slots && tiles % slots != 0 && tile.bn == 128) {
     int mode = 0;  // tuning override MDGEMM_STREAMK: 0 auto, 1 force on, -1 off
     if (const char* f = std::getenv("MDGEMM_STREAMK")) mode = std::atoi(f);
     // Only where the tail matters (few waves) and tiles are mainloop-bound:
@@ -314,21 +343,24 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   {
     const char* f = std::getenv("MDGEMM_STREAMK");
     const bool force = f && std::atoi(f) == 2;
-    if (!exact && splits == 1 && sk_grid == 0 && tiles > 0 &&
+    if (!exact && !dmma_ws && splits == 1 && sk_grid == 0 && tiles > 0 &&
         ((single && tile.bm == 128 && tile.bn == 128) || (force && tile.bn == 128)))
       sk_grid = static_cast<int>(tiles);
   }
+  // partial-tile slots and publish flags only where ranges split tiles
+  const bool sk_ranges = sk_grid > 0 && tiles % sk_grid != 0;
   const size_t acc_size = single ? sizeof(float) : sizeof(double);
   const size_t off_b = (pa.bytes + 255) / 256 * 256;
   const size_t off_p = off_b + (pb.bytes + 255) / 256 * 256;
   const size_t part_bytes = splits > 1 ? static_cast<size_t>(splits * tiles * tile.bm * tile.bn) * acc_size
-                                       : static_cast<size_t>(sk_grid) * tile.bm * tile.bn * acc_size;
+                            : sk_ranges ? static_cast<size_t>(sk_grid) * tile.bm * tile.bn * acc_size
+                                        : 0;
   const size_t off_f = off_p + (part_bytes + 255) / 256 * 256;
-  const size_t flag_bytes = static_cast<size_t>(sk_grid) * sizeof(int);  // stream-K publish flags
+  const size_t flag_bytes = sk_ranges ? static_cast<size_t>(sk_grid) * sizeof(int) : 0;  // publish flags
   void* ws = nullptr;
   cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
   char* wsa = static_cast<char*>(ws);
-  cudaError_t err = sk_grid > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
+  cudaError_t err = flag_bytes > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
   cuda_check(err, "stream-K flags");
   {
     prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes));
@@ -373,8 +405,8 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   g.kb_per_split = kb_per_split;
   g.partials = splits > 1 ? wsa + off_p : nullptr;
   g.sk_grid = sk_grid;
-  g.sk_partials = sk_grid > 0 ? wsa + off_p : nullptr;
-  g.sk_flags = sk_grid > 0 ? reinterpret_cast<int*>(wsa + off_f) : nullptr;
+  g.sk_partials = sk_ranges ? wsa + off_p : nullptr;
+  g.sk_flags = sk_ranges ? reinterpret_cast<int*>(wsa + off_f) : nullptr;
   g.prefetch = 0;
   g.c_prefetch = nk <= 16 ? 1 : 0;  // short k: the epilogue's C traffic is the critical path
   if (const char* force = std::getenv("MDGEMM_C_PREFETCH")) g.c_prefetch = std::atoi(force);
@@ -404,13 +436,15 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     } else {
       const int kind = single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA;
       const char* trace_path = std::getenv("MDGEMM_TRACE");  // tuning: per-CTA timeline of every gemm kernel
-      const int64_t grid = sk_grid > 0 ? mdg::sk_launch_grid(tiles, sk_grid) : tiles * splits;
+      const int64_t grid = dmma_ws ? ws_grid : sk_grid > 0 ? mdg::sk_launch_grid(tiles, sk_grid) : tiles * splits;
       if (trace_path && grid > 0 && err == cudaSuccess)
         err = cudaMallocAsync(reinterpret_cast<void**>(&g.trace), grid * mdg::TRACE_WORDS * 8, st);
       {
         prof::Scope scope(kind, st, 2.0 * p.m * p.n * p.k);
         if (err == cudaSuccess)
-          err = single ? mdg::launch_gemm_ffma(g, tile, st) : mdg::launch_gemm_dmma(g, tile, st);
+          err = dmma_ws  ? mdg::launch_gemm_dmma_ws(g, ws_grid, st)
+                : single ? mdg::launch_gemm_ffma(g, tile, st)
+                         : mdg::launch_gemm_dmma(g, tile, st);
       }
       if (g.trace) {
         std::vector<unsigned long long> h(static_cast<size_t>(grid) * mdg::TRACE_WORDS);

@@ -3,6 +3,7 @@
 // shapes), FP32 FFMA (SIMT).  Every kernel runs independent dependency chains
 // so the pipe, not latency, is the limit.  Prints one JSON object.
 #include <cstdio>
+#include <string>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
@@ -172,6 +173,22 @@ int main(int argc, char** argv) {
   double* dout; float* fout;
   CK(cudaMalloc(&dout, 64)); CK(cudaMalloc(&fout, 64));
   int reps = argc > 1 ? atoi(argv[1]) : 20;
+  if (argc > 2 && std::string(argv[2]) == "occ") {  // pipe rate vs resident warps per SM
+    printf("{\"sms\": %d", sms);
+    const int cfgs[][2] = {{1, 4}, {1, 8}, {2, 4}, {1, 12}, {3, 4}, {1, 16}};
+    for (auto& c : cfgs) {
+      dim3 grid(sms * c[0]), block(32 * c[1]);
+      double nwarps = double(grid.x) * c[1];
+      float ms = time_it([&] { k_dmma_884<<<grid, block>>>(dout); }, reps);
+      printf(", \"dmma884_%dcta_%dw_tflops\": %.3f", c[0], c[1],
+             nwarps * (ITERS / 4) * 8 * (8 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
+      double nthr = double(grid.x) * block.x;
+      ms = time_it([&] { k_ffma2<<<grid, block>>>(fout, 0.999f); }, reps);
+      printf(", \"ffma2_%dcta_%dw_tflops\": %.3f", c[0], c[1], nthr * ITERS * 8 * 4 / (ms * 1e-3) / 1e12);
+    }
+    printf("}\n");
+    return 0;
+  }
   printf("{\"sms\": %d, \"clock_khz_attr\": %d", sms, clk);
   for (int wpb : {4, 8, 16}) {
     dim3 grid(sms * 4), block(32 * wpb);
