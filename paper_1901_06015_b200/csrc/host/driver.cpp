@@ -332,7 +332,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     // with a short k the epilogue dominates and the stream-K variant's
     // heavier epilogue costs more than the tail (cfg5 k=64: -43 %).
     const double tail = static_cast<double>(tiles % slots) / static_cast<double>(slots);
-    const bool wins = tail < 0.85 && tiles < 16 * slots && nk >= 32;
+    const bool wins = tail < 0.85 && tiles < 8 * slots && nk >= 32;  // (13.8 waves: -2 %)
     if (mode == 1 || (mode == 0 && !shared && wins)) sk_grid = static_cast<int>(slots);
   }
   // The segment-loop kernel with one whole tile per CTA (sk_grid = tiles:
