@@ -130,6 +130,8 @@ cudaError_t launch_gemm_ffma(const GemmDesc& d, const FastTile& t, cudaStream_t 
 // `grid` CTAs (one per SM); d.sk_grid = grid turns on the stream-K tail.
 size_t dmma_ws_smem(int cdt);
 cudaError_t launch_gemm_dmma_ws(const GemmDesc& d, int grid, cudaStream_t s);
+size_t ffma_ws_smem(int cdt);
+cudaError_t launch_gemm_ffma_ws(const GemmDesc& d, int grid, cudaStream_t s);
 // Resident CTAs per SM of the kernel a tile shape / C datatype launches
 // (occupancy query; sizes the split-K and stream-K grids).
 int dmma_ctas_per_sm(const FastTile& t, int cdt);

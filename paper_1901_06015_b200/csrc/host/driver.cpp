@@ -270,20 +270,22 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
 
   mdg::FastTile tile{64, 64, 1};
   if (!exact) tile = single ? mdg::choose_ffma_tile(p.m, p.n, sms) : mdg::choose_dmma_tile(p.m, p.n, sms);
-  // Warp-specialised persistent DMMA kernel (gemm_dmma_ws.cu): 128x128 tiles,
-  // one CTA per SM, the epilogue of one tile under the next tile's mainloop.
-  bool dmma_ws = false;
-  if (!exact && !single) {
-    int mode = 0;  // MDGEMM_DMMA_WS: 1 force on (where it applies), -1 off, 0 auto
-    if (const char* f = std::getenv("MDGEMM_DMMA_WS")) mode = std::atoi(f);
+  // Warp-specialised persistent kernels (gemm_{dmma,ffma}_ws.cu): 128x128
+  // tiles, one CTA per SM, the C traffic of one tile under the next tile's
+  // mainloop.
+  bool dmma_ws = false;  // (either computation precision)
+  if (!exact) {
+    int mode = 0;  // MDGEMM_{DMMA,FFMA}_WS: 1 force on (where it applies), -1 off, 0 auto
+    if (const char* f = std::getenv(single ? "MDGEMM_FFMA_WS" : "MDGEMM_DMMA_WS")) mode = std::atoi(f);
     const int64_t t128 = ((p.m + 127) / 128) * ((p.n + 127) / 128);
     mdg::DEpilogue probe{};  // the kernel moves C only through a TMA tensor map
     probe.out = to_dview(p.c);
     probe.pair = static_cast<int32_t>(p.pair_axis);
     const bool complex_c = probe.out.dtype == MDG_DT_C || probe.out.dtype == MDG_DT_Z;
     const bool c_ok = encode_c_map(probe, 128) && (!complex_c || probe.pair != MDG_PAIR_NONE);
-    // auto: real C (measured +1..7 % over the classic kernel at the cfg2
-    // sizes 2048-4096; complex C -1..2 %), one full wave of 128x128 tiles,
+    // auto: real C (measured at the cfg2 sizes 2048-4096: DMMA +1..7 %,
+    // FFMA +2..4 %, short k far more -- rank-64 ssss 19.6 -> 27.3 TFLOP/s;
+    // complex C -1..2 %), one full wave of 128x128 tiles,
     // and the GPU to itself (a persistent grid inside a concurrent batch
     // would wait for slots the other calls hold; MDGEMM_DMMA_WS=2 allows it)
     const bool want = mode == 1 || (mode == 0 && !complex_c && !shared) || (mode == 2 && !complex_c);
@@ -442,7 +444,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
       {
         prof::Scope scope(kind, st, 2.0 * p.m * p.n * p.k);
         if (err == cudaSuccess)
-          err = dmma_ws  ? mdg::launch_gemm_dmma_ws(g, ws_grid, st)
+          err = dmma_ws  ? (single ? mdg::launch_gemm_ffma_ws(g, ws_grid, st) : mdg::launch_gemm_dmma_ws(g, ws_grid, st))
                 : single ? mdg::launch_gemm_ffma(g, tile, st)
                          : mdg::launch_gemm_dmma(g, tile, st);
       }

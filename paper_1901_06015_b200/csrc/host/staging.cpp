@@ -16,6 +16,7 @@
 // versa), and host inputs that an earlier call's copy-out writes are read
 // only after that copy-out.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -122,6 +123,12 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     size_t staged = 0;  // host-staged calls issued so far (for the in-flight throttle)
     std::vector<size_t> staged_ids;
     int rr = 0;
+    static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..4 concurrent compute streams
+      const char* f = std::getenv("MDGEMM_STREAMS");
+      const int v = f ? std::atoi(f) : kComputeStreams;
+      return v < 1 ? 1 : (v > kComputeStreams ? kComputeStreams : v);
+    }();
+    double queued[kComputeStreams] = {};  // estimated work placed on each compute stream
     for (size_t i = 0; i < calls.size(); ++i) {
       Call& c = cs[i];
       ExecutionPlan& p = c.plan;
@@ -156,7 +163,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
       long latest[kComputeStreams];
       std::fill(latest, latest + kComputeStreams, -1L);
       long newest = -1;
-      int unresolved = kComputeStreams;
+      int unresolved = nstreams;
       for (long h = static_cast<long>(i) - 1; h >= 0 && unresolved > 0; --h) {
         const Call& e = cs[static_cast<size_t>(h)];
         if (latest[e.stream] >= 0 || !conflicts(e)) continue;
@@ -166,10 +173,19 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
       }
       if (newest >= 0) {
         c.stream = cs[static_cast<size_t>(newest)].stream;
-      } else {
+      } else {  // a new chain: the stream with the least queued work (ties round-robin)
         c.stream = rr;
-        rr = (rr + 1) % kComputeStreams;
+        for (int q = 1; q < nstreams; ++q) {
+          const int s = (rr + q) % nstreams;
+          if (queued[s] < queued[c.stream]) c.stream = s;
+        }
+        rr = (rr + 1) % nstreams;
       }
+      // estimated device time of the call: useful flops at its pipe's rate
+      // (FP32 FFMA2 about twice the FP64 DMMA rate) plus the operand bytes
+      queued[c.stream] += (p.comp_prec == Precision::Single ? 0.5 : 1.0) * static_cast<double>(p.m) *
+                              static_cast<double>(p.n) * static_cast<double>(p.k) +
+                          1e3 * static_cast<double>(p.m + p.n);
       cudaStream_t cst = S.compute[c.stream];
 
       // ---- copy-in of host operands

@@ -50,3 +50,19 @@ def test_ws_against_oracle(beta, monkeypatch):
     va, vb, vc = p.views()
     _, _, va_after = p.views(C=after)
     assert O.orc_violation(SCALARS["p7"], va, vb, SCALARS[beta], vc, va_after, p.comp) <= 1.0
+
+
+@pytest.mark.parametrize("label", ["ssss", "dsss", "cccs", "cdzs", "zdzs", "szzs", "sdds", "csds"])
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("streamk", ["0", "-1"])
+def test_ffma_ws_bitwise_equals_classic(label, shape, streamk, monkeypatch):
+    m, n, k = shape
+    cid = M.CaseLabel.parse(label).case_id()
+    if cid == 7:
+        m = m // 2
+    p = Problem(label, m, n, k, seed=19)
+    alpha = SCALARS["cfg3_alpha"] if cid == 7 else SCALARS["p7"]
+    beta = SCALARS["cfg2_beta"]
+    classic = run(p, alpha, beta, {"MDGEMM_FFMA_WS": "-1", "MDGEMM_STREAMK": "-1"}, monkeypatch)
+    ws = run(p, alpha, beta, {"MDGEMM_FFMA_WS": "1", "MDGEMM_STREAMK": streamk}, monkeypatch)
+    assert np.array_equal(classic, ws)
