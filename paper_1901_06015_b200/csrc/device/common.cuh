@@ -386,80 +386,109 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
   const int64_t om = prow ? e.me / 2 : e.me, on = pcol ? e.ne / 2 : e.ne;  // output extent
   const bool reads_c = !e.beta.is_zero;
   const bool conj = e.out.conj != 0;
-  const uint32_t col_bytes = orows * O::ESZ;
   R* const out = reinterpret_cast<R*>(e.out.base);
+  // The tile is staged in "lines" along C's contiguous dimension: columns for
+  // a column-major C (cmap_ok 1, and 3 = the real part of an interleaved
+  // complex C), rows for a row-major one (2: a transposed plan).  With a TMA
+  // tensor map, C moves as boxes of C_BOX_COLS lines (loads into cbuf, stores
+  // from tbuf -- or from cbuf for a real part, whose imaginary halves go back
+  // unchanged); the map clips edge tiles.  Chunks are whole boxes that fit
+  // beside the staged tile.
+  const int cmode = e.cmap_ok;
+  const bool rowm = cmode == MDG_CMAP_ROWS;
+  const bool halfc = cmode == MDG_CMAP_REAL_PART;
+  const int nlines = rowm ? orows : ocols, llen = rowm ? ocols : orows;
+  const uint32_t line_bytes = llen * O::ESZ;
+  const uint32_t cline_bytes = halfc ? 2 * line_bytes : line_bytes;
+  auto sidx = [&](int oi, int oj) { return rowm ? oi * ocols + oj : oj * orows + oi; };
   unsigned char* tbuf = smem;
-  unsigned char* cbuf = smem + ocols * col_bytes;
-  // TMA path: C moves as 2-D tensor boxes of C_BOX_COLS columns (loads into
-  // cbuf, results written back into tbuf and stored from there); the tensor
-  // map clips edge tiles.  Chunks are whole boxes that fit beside the tile.
-  const int CH_FIT = static_cast<int>((region - ocols * col_bytes) / col_bytes) / C_BOX_COLS * C_BOX_COLS;
-  const bool tma = e.cmap_ok != 0 && CH_FIT >= C_BOX_COLS;
-  const int CH = tma ? min(ocols, CH_FIT) : ocols;
+  unsigned char* cbuf = smem + nlines * line_bytes;
+  const int CH_FIT = static_cast<int>((region - nlines * line_bytes) / cline_bytes) / C_BOX_COLS * C_BOX_COLS;
+  const bool tma = cmode != 0 && CH_FIT >= C_BOX_COLS;
+  const bool loads = tma && (reads_c || halfc);  // a real part always needs the imaginary halves
+  const int CH = tma ? min(nlines, CH_FIT) : nlines;
   const CUtensorMap* map = &e.cmap;
-  const int x0 = static_cast<int>(oi0 * NC);
-  auto load_chunk = [&](int j0) {
-    const int nb = (min(CH, ocols - j0) + C_BOX_COLS - 1) / C_BOX_COLS;
+  const int x0 = static_cast<int>(rowm ? oj0 * NC : (halfc ? 2 * oi0 : oi0 * NC));
+  const int64_t line0 = rowm ? oi0 : oj0;
+  auto load_chunk = [&](int l0) {
+    const int nb = (min(CH, nlines - l0) + C_BOX_COLS - 1) / C_BOX_COLS;
     fence_proxy_async();
-    mbar_arrive_expect_tx(cbar, nb * C_BOX_COLS * col_bytes);
+    mbar_arrive_expect_tx(cbar, nb * C_BOX_COLS * cline_bytes);
     for (int b = 0; b < nb; ++b)
-      tensor_load_2d(cbuf + b * C_BOX_COLS * col_bytes, map, x0, static_cast<int>(oj0 + j0 + b * C_BOX_COLS), cbar);
+      tensor_load_2d(cbuf + b * C_BOX_COLS * cline_bytes, map, x0, static_cast<int>(line0 + l0 + b * C_BOX_COLS), cbar);
   };
-  if (tma && reads_c && tid == 0) load_chunk(0);
+  if (loads && tid == 0) load_chunk(0);
   emit([&](int r, int c, double v) {
     const int oi = prow ? r >> 1 : r, oj = pcol ? c >> 1 : c;
     const int comp = prow ? (r & 1) : (pcol ? (c & 1) : 0);
-    reinterpret_cast<R*>(tbuf)[(oj * orows + oi) * NC + comp] = static_cast<R>(v);
+    reinterpret_cast<R*>(tbuf)[sidx(oi, oj) * NC + comp] = static_cast<R>(v);
   });
   named_sync(1, nthr);
 
-  for (int j0 = 0; j0 < ocols; j0 += CH) {
-    const int ch = min(CH, ocols - j0);
-    if (tma) {
-      if (reads_c) {
-        mbar_wait(cbar, phase);
-        phase ^= 1;
-      }
-      const int nv = ch * orows / VEC;
+  if (!tma) {  // element-wise through C's strides
+    const int n = orows * ocols;
+    for (int idx = tid; idx < n; idx += nthr) {
+      const int oi = idx % orows, oj = idx / orows;
+      const int64_t gi = oi0 + oi, gj = oj0 + oj;
+      if (gi >= om || gj >= on) continue;
+      R* cp = out + (gi * e.out.rs + gj * e.out.cs) * NC;
+      R cv[NC];
+      const R* tp = reinterpret_cast<const R*>(tbuf) + static_cast<size_t>(sidx(oi, oj)) * NC;
+#pragma unroll
+      for (int u = 0; u < NC; ++u) cv[u] = reads_c ? cp[u] : R(0);
+      combine_typed<CDT>(e.beta, conj, cv, tp);
+#pragma unroll
+      for (int u = 0; u < NC; ++u) cp[u] = cv[u];
+    }
+    return;
+  }
+  for (int l0 = 0; l0 < nlines; l0 += CH) {
+    const int ch = min(CH, nlines - l0);
+    if (loads) {
+      mbar_wait(cbar, phase);
+      phase ^= 1;
+    }
+    if (!halfc) {
+      const int nv = ch * llen / VEC;
       for (int v = tid; v < nv; v += nthr) {
-        const int idx = v * VEC;  // element within the chunk, column-major
+        const int idx = v * VEC;  // element within the chunk, line-major
         union {
           uint4 u;
           R x[VEC * NC];
         } cv, tv;
-        uint4* tp = reinterpret_cast<uint4*>(tbuf + (static_cast<size_t>(j0) * orows + idx) * O::ESZ);
+        uint4* tp = reinterpret_cast<uint4*>(tbuf + (static_cast<size_t>(l0) * llen + idx) * O::ESZ);
         tv.u = *tp;
         cv.u = reads_c ? *reinterpret_cast<const uint4*>(cbuf + static_cast<size_t>(idx) * O::ESZ) : make_uint4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < VEC; ++u) combine_typed<CDT>(e.beta, conj, &cv.x[u * NC], &tv.x[u * NC]);
         *tp = cv.u;
       }
-      fence_proxy_async();  // generic writes of tbuf before the async-proxy store reads them
-      named_sync(1, nthr);  // ... and every thread is done with cbuf
-      if (tid == 0) {
-        for (int b = 0; b < ch; b += C_BOX_COLS)
-          tensor_store_2d(map, x0, static_cast<int>(oj0 + j0 + b), tbuf + static_cast<size_t>(j0 + b) * col_bytes);
-        bulk_commit();
-        if (reads_c && j0 + ch < ocols) load_chunk(j0 + ch);
-      }
-    } else {
-      const int n = ch * orows;
+    } else {  // real part: combine into the even slots of the interleaved chunk
+      const int n = ch * llen;
+      R* cb = reinterpret_cast<R*>(cbuf);
+      const R* tb = reinterpret_cast<const R*>(tbuf) + static_cast<size_t>(l0) * llen;
       for (int idx = tid; idx < n; idx += nthr) {
-        const int oi = idx % orows, oj = idx / orows;
-        const int64_t gi = oi0 + oi, gj = oj0 + j0 + oj;
-        if (gi >= om || gj >= on) continue;
-        R* cp = out + (gi * e.out.rs + gj * e.out.cs) * NC;
-        R cv[NC];
-        const R* tp = reinterpret_cast<const R*>(tbuf) + (static_cast<size_t>(j0) * orows + idx) * NC;
-#pragma unroll
-        for (int u = 0; u < NC; ++u) cv[u] = reads_c ? cp[u] : R(0);
-        combine_typed<CDT>(e.beta, conj, cv, tp);
-#pragma unroll
-        for (int u = 0; u < NC; ++u) cp[u] = cv[u];
+        R cv = reads_c ? cb[2 * idx] : R(0);
+        combine_typed<CDT>(e.beta, conj, &cv, &tb[idx]);
+        cb[2 * idx] = cv;
+      }
+    }
+    fence_proxy_async();  // generic writes before the async-proxy store reads them
+    named_sync(1, nthr);  // ... and every thread is done with this chunk
+    if (tid == 0) {
+      for (int b = 0; b < ch; b += C_BOX_COLS) {
+        const unsigned char* src = halfc ? cbuf + static_cast<size_t>(b) * cline_bytes
+                                         : tbuf + static_cast<size_t>(l0 + b) * line_bytes;
+        tensor_store_2d(map, x0, static_cast<int>(line0 + l0 + b), src);
+      }
+      bulk_commit();
+      if (l0 + ch < nlines) {
+        if (halfc) bulk_wait_read();  // the next chunk lands where this one is being stored from
+        if (loads) load_chunk(l0 + ch);
       }
     }
   }
-  if (tma && tid == 0) bulk_wait_read();  // the stores have read tbuf: the smem may be reused / released
+  if (tid == 0) bulk_wait_read();  // the stores have read the smem: it may be reused / released
 }
 
 // Grouped tile raster: walks `group` tile-rows at a time.  A short group

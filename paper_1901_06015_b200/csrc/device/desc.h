@@ -40,7 +40,15 @@ struct DEpilogue {
   DBeta beta;
   int64_t me, ne;
 };
-constexpr int C_BOX_COLS = 16;
+constexpr int C_BOX_COLS = 16;  // lines (columns, or rows for MDG_CMAP_ROWS) per TMA box
+// DEpilogue::cmap_ok: how the tensor map covers C
+enum : int32_t {
+  MDG_CMAP_NONE = 0,       // no map: element-wise epilogue
+  MDG_CMAP_COLS = 1,       // column-major C (rs == 1)
+  MDG_CMAP_ROWS = 2,       // row-major C (cs == 1): a transposed plan
+  MDG_CMAP_REAL_PART = 3,  // real view with rs == 2 (real part of an interleaved complex C); the map
+                           // covers both halves and the other half is written back unchanged
+};
 
 // Panel geometry of one packed operand, in real elements of the computation
 // precision: panels of `pd` rows (left) / columns (right), `lpad` inner-

@@ -186,11 +186,16 @@ std::size_t packed_bytes(const MatrixView& src, Side side, PackFormat format, Da
   return pack_geometry(src, side, format, target, reg_block, 0).bytes;
 }
 
-// C as a 2-D TMA tensor for the fused epilogue (common.cuh: fast_epilogue):
-// inner dimension = rows x components in C's real type, outer = columns,
-// boxes of (tile rows) x C_BOX_COLS.  Column-major C with 16-byte aligned
-// columns only; anything else keeps the element-wise epilogue path.
-static bool encode_c_map(mdg::DEpilogue& e, int bm) {
+// C as a 2-D TMA tensor for the fused epilogue (common.cuh: fast_epilogue),
+// boxes of (tile extent along C's contiguous dimension) x C_BOX_COLS lines.
+// Returns the MDG_CMAP_* mode (0: none; the element-wise epilogue then):
+//   COLS       column-major C: inner = rows x components, outer = columns;
+//   ROWS       row-major C (a transposed plan): inner = columns x components,
+//              outer = rows;
+//   REAL_PART  a real view with rs == 2 (the real part of an interleaved
+//              complex C, case 1c): inner = both halves of each row pair.
+// All need 16-byte aligned base and line strides.
+static int encode_c_map(mdg::DEpilogue& e, int bm, int bn) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -202,22 +207,47 @@ static bool encode_c_map(mdg::DEpilogue& e, int bm) {
       return static_cast<Encode>(nullptr);
     return reinterpret_cast<Encode>(fn);
   }();
-  if (!encode) return false;
+  if (!encode) return mdg::MDG_CMAP_NONE;
   const bool single = e.out.dtype == MDG_DT_S || e.out.dtype == MDG_DT_C;
   const int nc = (e.out.dtype == MDG_DT_C || e.out.dtype == MDG_DT_Z) ? 2 : 1;
-  const int esz = (single ? 4 : 8) * nc;
-  const int orows = e.pair == MDG_PAIR_ROWS ? bm / 2 : bm;
+  const int esr = single ? 4 : 8, esz = esr * nc;
+  const int orows = e.pair == MDG_PAIR_ROWS ? bm / 2 : bm, ocols = e.pair == MDG_PAIR_COLS ? bn / 2 : bn;
   const auto base = reinterpret_cast<uintptr_t>(e.out.base);
-  if (e.out.rs != 1 || e.out.m <= 0 || e.out.n <= 0 || base % 16 || (e.out.cs * esz) % 16 || (orows * esz) % 16 ||
-      orows * nc > 256)
-    return false;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(e.out.m * nc), static_cast<cuuint64_t>(e.out.n)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.out.cs * esz)};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(orows * nc), static_cast<cuuint32_t>(mdg::C_BOX_COLS)};
+  if (e.out.m <= 0 || e.out.n <= 0 || base % 16) return mdg::MDG_CMAP_NONE;
+  int mode = mdg::MDG_CMAP_NONE;
+  cuuint64_t dims[2];
+  cuuint64_t stride = 0;
+  cuuint32_t inner = 0;
+  if (e.out.rs == 1) {
+    mode = mdg::MDG_CMAP_COLS;
+    dims[0] = static_cast<cuuint64_t>(e.out.m * nc);
+    dims[1] = static_cast<cuuint64_t>(e.out.n);
+    stride = static_cast<cuuint64_t>(e.out.cs * esz);
+    inner = static_cast<cuuint32_t>(orows * nc);
+  } else if (e.out.cs == 1) {
+    mode = mdg::MDG_CMAP_ROWS;
+    dims[0] = static_cast<cuuint64_t>(e.out.n * nc);
+    dims[1] = static_cast<cuuint64_t>(e.out.m);
+    stride = static_cast<cuuint64_t>(e.out.rs * esz);
+    inner = static_cast<cuuint32_t>(ocols * nc);
+  } else if (e.out.rs == 2 && nc == 1) {
+    mode = mdg::MDG_CMAP_REAL_PART;
+    dims[0] = static_cast<cuuint64_t>(2 * e.out.m);
+    dims[1] = static_cast<cuuint64_t>(e.out.n);
+    stride = static_cast<cuuint64_t>(e.out.cs * esr);
+    inner = static_cast<cuuint32_t>(2 * orows);
+  } else {
+    return mdg::MDG_CMAP_NONE;
+  }
+  if (stride % 16 || (inner * esr) % 16 || inner > 256) return mdg::MDG_CMAP_NONE;
+  const cuuint64_t strides[1] = {stride};
+  const cuuint32_t box[2] = {inner, static_cast<cuuint32_t>(mdg::C_BOX_COLS)};
   const cuuint32_t estride[2] = {1, 1};
-  return encode(&e.cmap, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
-                e.out.base, dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const bool ok = encode(&e.cmap, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                         e.out.base, dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return ok ? mode : mdg::MDG_CMAP_NONE;
 }
 
 // Resident CTAs per SM of a fast kernel (occupancy query, cached per
@@ -282,7 +312,8 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     probe.out = to_dview(p.c);
     probe.pair = static_cast<int32_t>(p.pair_axis);
     const bool complex_c = probe.out.dtype == MDG_DT_C || probe.out.dtype == MDG_DT_Z;
-    const bool c_ok = encode_c_map(probe, 128) && (!complex_c || probe.pair != MDG_PAIR_NONE);
+    const bool c_ok = encode_c_map(probe, 128, 128) == mdg::MDG_CMAP_COLS &&  // WS kernels: column-major C
+                      (!complex_c || probe.pair != MDG_PAIR_NONE);
     // auto: real C (measured at the cfg2 sizes 2048-4096: DMMA +1..7 %,
     // FFMA +2..4 %, short k far more -- rank-64 ssss 19.6 -> 27.3 TFLOP/s;
     // complex C -1..2 %), one full wave of 128x128 tiles,
@@ -384,7 +415,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   g.epi.beta = to_dbeta(p.beta);
   g.epi.me = p.m;
   g.epi.ne = p.n;
-  g.epi.cmap_ok = !exact && encode_c_map(g.epi, tile.bm) ? 1 : 0;
+  g.epi.cmap_ok = exact ? mdg::MDG_CMAP_NONE : encode_c_map(g.epi, tile.bm, tile.bn);
   if (const char* f = std::getenv("MDGEMM_C_TMA"))  // tuning: 0 = element-wise epilogue
     if (std::atoi(f) == 0) g.epi.cmap_ok = 0;
   g.kc = p.params.kc;
