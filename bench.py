@@ -243,12 +243,14 @@ def run_b200(args):
         dist.barrier()
     sampler = ClockSampler(local)
     launches0 = M.launch_count()
-    step_ms = []
+    step_ms, enqueue_ms = [], []
     for _ in range(args.steps):
         flush.fill_(1)  # L2 flush between timed steps (outside the events)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         step()
+        enqueue_ms.append((time.perf_counter() - h0) * 1e3)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -406,6 +408,8 @@ def run_b200(args):
         "kernels": kernels,
         "per_case": per_case,
         "serialized_step_ms": serial_ms,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "host_enqueue_ms": [round(x, 1) for x in enqueue_ms],
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,

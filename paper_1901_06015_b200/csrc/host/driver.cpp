@@ -32,6 +32,11 @@ int device_sms() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = ~0ULL;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      // Never let an allocation on one compute stream wait for a free on
+      // another (the allocator would insert that dependency to reuse the
+      // block, serialising the concurrent calls of a batch): grow instead.
+      int no = 0;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     cache[dev] = sms;
   }
