@@ -36,7 +36,7 @@ bool is_device_ptr(const void* ptr) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
-constexpr int kComputeStreams = 4;
+constexpr int kComputeStreams = 8;  // at most; MDGEMM_STREAMS picks how many a batch uses
 constexpr size_t kDepth = 3;  // host-staged calls allowed in flight (bounds staging memory)
 
 // Per-device copy-in / compute / copy-out streams (blocking streams, so they
@@ -125,7 +125,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     int rr = 0;
     static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..4 concurrent compute streams
       const char* f = std::getenv("MDGEMM_STREAMS");
-      const int v = f ? std::atoi(f) : kComputeStreams;
+      const int v = f ? std::atoi(f) : 4;  // default four concurrent streams
       return v < 1 ? 1 : (v > kComputeStreams ? kComputeStreams : v);
     }();
     double queued[kComputeStreams] = {};  // estimated work placed on each compute stream

@@ -166,6 +166,49 @@ static float time_it(F launch, int reps) {
   return best;
 }
 
+// Co-residency probe: warps [0, dw) run the DMMA loop, the rest the FFMA2
+// loop, in one CTA -- do the FP64 tensor pipe and the FP32 FMA pipe overlap?
+__global__ void k_mix(double* dout, float* fout, int dw, int dit, int fit) {
+  const int warp = threadIdx.x >> 5;
+  if (warp < dw) {
+    double a[8], b[8], c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 1e-3 + i; b[i] = 0.5 + i; c[i][0] = c[i][1] = 0; }
+    for (int it = 0; it < dit; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[i]), "d"(b[i]));
+    }
+    double r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+    if (r == 1234.5) dout[0] = r;
+  } else {
+    unsigned long long acc[8], x[8];
+    float bv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float v = threadIdx.x * 1e-3f + i;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(acc[i]) : "f"(v), "f"(v + 1.0f));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(x[i]) : "f"(v * 0.5f), "f"(v * 0.25f));
+      bv[i] = 0.999f + i;
+    }
+    for (int it = 0; it < fit; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        unsigned long long b;
+        asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(bv[i]));
+        asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i]) : "l"(b), "l"(x[i]));
+      }
+    }
+    float r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += __uint_as_float(static_cast<unsigned>(acc[i]));
+    if (r == 1234.5f) fout[0] = r;
+  }
+}
+
 int main(int argc, char** argv) {
   int sms = 0, clk = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -173,6 +216,25 @@ int main(int argc, char** argv) {
   double* dout; float* fout;
   CK(cudaMalloc(&dout, 64)); CK(cudaMalloc(&fout, 64));
   int reps = argc > 1 ? atoi(argv[1]) : 20;
+  if (argc > 2 && std::string(argv[2]) == "mix") {  // DMMA and FFMA2 warps side by side
+    printf("{\"sms\": %d", sms);
+    // 8 DMMA warps + 8 FFMA2 warps per SM; iteration counts chosen so each
+    // alone would take about the same time at its peak
+    const int dit = 2048, fit = 8192;
+    // (DMMA warps, FFMA warps) per SM
+    const int cfgs[][2] = {{8, 0}, {0, 8}, {8, 8}, {4, 0}, {0, 4}, {4, 4}, {8, 4}, {4, 8}, {4, 12}};
+    for (auto& c : cfgs) {
+      const int dw = c[0], fw = c[1];
+      dim3 grid(sms), block(32 * (dw + fw));
+      float ms = time_it([&] { k_mix<<<grid, block>>>(dout, fout, dw, dit, fit); }, reps);
+      const double dfl = double(sms) * dw * dit * 8 * (8 * 8 * 4 * 2);
+      const double ffl = double(sms) * fw * 32 * fit * 8 * 4;
+      const double dt = dfl / (ms * 1e-3) / 1e12, ft = ffl / (ms * 1e-3) / 1e12;
+      printf(", \"d%d_f%d\": [%.2f, %.2f, %.3f]", dw, fw, dt, ft, dt / 37.0 + ft / 72.0);
+    }
+    printf("}\n");
+    return 0;
+  }
   if (argc > 2 && std::string(argv[2]) == "occ") {  // pipe rate vs resident warps per SM
     printf("{\"sms\": %d", sms);
     const int cfgs[][2] = {{1, 4}, {1, 8}, {2, 4}, {1, 12}, {3, 4}, {1, 16}};
