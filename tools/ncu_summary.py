@@ -17,8 +17,10 @@ ALGO = {
     "ffma": 8192 * 8192 * 4 + 8192 * 4096 * 4 + 2 * 4096 * 4096 * 8,
     # zzzd 1e pack of A: 4096^2 z read, 8192^2 f64 written
     "pack": 4096 * 4096 * 16 + 8192 * 8192 * 8,
+    # dddd 4096 on the warp-specialised kernel: A + B packed f64, C read + written
+    "dmma_ws": 4 * 4096 * 4096 * 8,
 }
-FLOPS = {"dmma": 2.0 * 8192 * 4096 * 8192, "ffma": 2.0 * 8192 * 4096 * 8192}
+FLOPS = {"dmma": 2.0 * 8192 * 4096 * 8192, "ffma": 2.0 * 8192 * 4096 * 8192, "dmma_ws": 2.0 * 4096 ** 3}
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA subpipe % active"),
@@ -48,12 +50,12 @@ def main():
     os.makedirs(dst, exist_ok=True)
     lines = ["# ncu --set full captures, round 1 (tools/profile_r01.sh, one launch each, --clock-control none)", "",
              "Launches: DMMA = `zzzd` 4096 (1m: me=8192, ne=4096, ke=8192), FFMA = `cccs` 4096 (same real dims), "
-             "pack = the 1e pack of `zzzd`'s A.  Per-launch times are cold-cache and serialised (ncu replays), so "
+             "pack = the 1e pack of `zzzd`'s A, dmma_ws = the warp-specialised DMMA kernel on a lone `dddd` 4096 call.  Per-launch times are cold-cache and serialised (ncu replays), so "
              "compare shares, not absolutes, with bench.py.", ""]
     traffic = {"what": "dram__bytes_read.sum + dram__bytes_write.sum of one captured launch (ncu --set full): "
                        "dmma = zzzd 4096, ffma = cccs 4096, pack = zzzd's 1e pack of A; algorithmic bytes alongside",
                "algorithmic_bytes_per_launch": {}}
-    for k in ("dmma", "ffma", "pack"):
+    for k in ("dmma", "ffma", "pack", "dmma_ws"):
         p = os.path.join(src, f"ncu_{k}_raw.csv")
         if not os.path.exists(p):
             continue

@@ -19,3 +19,10 @@ for spec in "dmma gemm_dmma zzzd" "ffma gemm_ffma cccs" "pack pack_kernel zzzd";
   ncu -i $O/prof_$1.ncu-rep --page raw --csv > $O/ncu_$1_raw.csv 2>/dev/null
   ncu -i $O/prof_$1.ncu-rep --page details --csv > $O/ncu_$1_details.csv 2>/dev/null
 done
+# the warp-specialised persistent DMMA kernel (lone call, real C): dddd 4096
+C2="python tools/exp_shape.py dddd 4096 4096 4096"
+$C2 > $O/plain_ws.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gemm_dmma_ws -s 1 -c 1 -o $O/prof_dmma_ws -f $C2 > $O/ncu_dmma_ws.log 2>&1
+echo dmma_ws_rc=$?
+ncu -i $O/prof_dmma_ws.ncu-rep --page raw --csv > $O/ncu_dmma_ws_raw.csv 2>/dev/null
+ncu -i $O/prof_dmma_ws.ncu-rep --page details --csv > $O/ncu_dmma_ws_details.csv 2>/dev/null
