@@ -90,15 +90,18 @@ __device__ __forceinline__ WsSched ws_sched(int64_t tiles, int nk, bool sk) {
   return s;
 }
 
-// Order: SEG_START first (the next CTA's SEG_END waits for it), whole tiles,
-// the range's whole tiles, SEG_END last.
+// Order: the whole-tile waves first, so every CTA runs them in step (the
+// wave's CTAs then share each A/B slab in L2 -- a START segment of varying
+// length up front would offset them by up to a tile), then SEG_START, the
+// range's whole tiles, SEG_END last.  CTA b+1 reaches its SEG_END no earlier
+// than CTA b finishes its SEG_START, since every range is >= one tile long.
 __device__ __forceinline__ Seg ws_seg(const WsSched& s, int idx) {
+  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
+  idx -= s.dpw;
   if (s.start_k1 != 0) {
     if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
     --idx;
   }
-  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
-  idx -= s.dpw;
   if (idx < s.full1 - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
   return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
 }
@@ -225,11 +228,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
   const int tid = threadIdx.x;
   const int wm = warp % WS_WM, wn = warp / WS_WM;
   const int g = lane >> 2, tig = lane & 3;
-  const bool conj = e.out.conj != 0;
   const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
   const double* a_base = sA + wm * 64 + g + tig * WS_BM;
   const double* b_base = sB + wn * 32 + g + tig * WS_BN;
-  R* const ct = reinterpret_cast<R*>(ctile);
   int it = 0, epis = 0;
   for (int si = 0; si < sc.nseg; ++si) {
     const Seg sg = ws_seg(sc, si);
@@ -286,8 +287,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
       continue;
     }
-    // combine with this tile's C (already in ctile) in place
+    // combine with this tile's C (already in ctile) in place.  The epilogue
+    // parameters are re-read here through an opaque pointer: hoisted above
+    // the segment loop they would stay live through the mainloop, which runs
+    // at the register cap (168).
     mbar_wait(c_full, epis & 1);
+    const DEpilogue* ep = &d.epi;
+    asm volatile("" : "+l"(ep));
+    const bool eprow = ep->pair == MDG_PAIR_ROWS, epcol = ep->pair == MDG_PAIR_COLS;
+    const int eorows = eprow ? WS_BM / 2 : WS_BM;
+    const bool ereads = !ep->beta.is_zero, econj = ep->out.conj != 0;
+    R* const ect = reinterpret_cast<R*>(smem + W::RING);
 #pragma unroll
     for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
@@ -297,10 +307,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
         if constexpr (NC == 1) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            R* p = ct + (c + h) * orows + r;
-            R cv = reads_c ? *p : R(0);
+            R* p = ect + (c + h) * eorows + r;
+            R cv = ereads ? *p : R(0);
             const R tv = static_cast<R>(h ? a1 : a0);
-            combine_typed<CDT>(e.beta, conj, &cv, &tv);
+            combine_typed<CDT>(ep->beta, econj, &cv, &tv);
             *p = cv;
           }
         } else {
@@ -309,23 +319,23 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
           // g, (r/2, c+1) for odd g after one exchange)
           R tv[2];
           R* p;
-          if (pcol) {
+          if (epcol) {
             tv[0] = static_cast<R>(a0);
             tv[1] = static_cast<R>(a1);
-            p = ct + ((c >> 1) * orows + r) * 2;
+            p = ect + ((c >> 1) * eorows + r) * 2;
           } else {
             const double other = __shfl_xor_sync(0xffffffffu, (g & 1) ? a0 : a1, 4);
             const bool odd = g & 1;
             tv[0] = static_cast<R>(odd ? other : a0);
             tv[1] = static_cast<R>(odd ? a1 : other);
-            p = ct + ((odd ? c + 1 : c) * orows + (r >> 1)) * 2;
+            p = ect + ((odd ? c + 1 : c) * eorows + (r >> 1)) * 2;
           }
           R cv[2] = {R(0), R(0)};
-          if (reads_c) {
+          if (ereads) {
             cv[0] = p[0];
             cv[1] = p[1];
           }
-          combine_typed<CDT>(e.beta, conj, cv, tv);
+          combine_typed<CDT>(ep->beta, econj, cv, tv);
           p[0] = cv[0];
           p[1] = cv[1];
         }

@@ -74,13 +74,15 @@ __device__ __forceinline__ FwSched fw_sched(int64_t tiles, int nk, bool sk) {
   return s;
 }
 
+// whole-tile waves first (in step across CTAs), then the stream-K range
+// (see gemm_dmma_ws.cu: ws_seg)
 __device__ __forceinline__ Seg fw_seg(const FwSched& s, int idx) {
+  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
+  idx -= s.dpw;
   if (s.start_k1 != 0) {
     if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
     --idx;
   }
-  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
-  idx -= s.dpw;
   if (idx < s.full1 - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
   return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
 }
