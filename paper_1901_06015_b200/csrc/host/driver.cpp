@@ -37,6 +37,16 @@ int device_sms() {
       // block, serialising the concurrent calls of a batch): grow instead.
       int no = 0;
       cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+      // Optional up-front reservation (MDGEMM_POOL_RESERVE_GB): growing the
+      // pool maps new memory in the middle of a batch.
+      if (const char* f = std::getenv("MDGEMM_POOL_RESERVE_GB")) {
+        const double gb = std::atof(f);
+        void* p = nullptr;
+        if (gb > 0 && cudaMallocAsync(&p, static_cast<size_t>(gb * (1ull << 30)), cudaStreamLegacy) == cudaSuccess) {
+          cudaFreeAsync(p, cudaStreamLegacy);
+          cudaStreamSynchronize(cudaStreamLegacy);
+        }
+      }
     }
     cache[dev] = sms;
   }
@@ -273,8 +283,16 @@ void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCo
   execute_scheduled(p, numerics, stream_ptr, fc, false);
 }
 
-void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared) {
+size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared) {
+  size_t n = 0;
+  execute_scheduled(p, numerics, nullptr, nullptr, shared, nullptr, 0, &n);
+  return n;
+}
+
+void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared,
+                       void* arena, size_t arena_bytes, size_t* ws_needed) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
+  if (ws_needed) *ws_needed = 0;
   if (p.m == 0 || p.n == 0) return;
   // Device-ordered entry points need device operands; a host pointer here
   // would fault inside a kernel and poison the context, so refuse it.
@@ -287,12 +305,15 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
       throw Error(std::string("execute: operand ") + what +
                   " is not in device memory (use gemm()/gemm_batch() for host operands)");
   };
-  require_device(p.c, "C");
-  if (p.k > 0) {
-    require_device(p.a, "A");
-    require_device(p.b, "B");
+  if (!ws_needed) {  // (a workspace query may see host operands that are staged later)
+    require_device(p.c, "C");
+    if (p.k > 0) {
+      require_device(p.a, "A");
+      require_device(p.b, "B");
+    }
   }
   if (p.k == 0) {
+    if (ws_needed) return;
     if (!p.beta.is_one()) {
       prof::Scope scope(MDG_KERNEL_BETA, st, 2.0 * p.c.m * p.c.n * dtype_size(p.c.dtype));
       cuda_check(mdg::launch_beta_pass(to_dview(p.c), to_dbeta(p.beta), st), "beta pass");
@@ -395,8 +416,19 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
                                         : 0;
   const size_t off_f = off_p + (part_bytes + 255) / 256 * 256;
   const size_t flag_bytes = sk_ranges ? static_cast<size_t>(sk_grid) * sizeof(int) : 0;  // publish flags
+  if (ws_needed) {
+    *ws_needed = off_f + flag_bytes;
+    return;
+  }
+  // The caller's arena (gemm_batch: one per compute stream, reused by the
+  // stream's calls in stream order) or a stream-ordered pool allocation.
   void* ws = nullptr;
-  cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
+  const bool owned = !(arena && arena_bytes >= off_f + flag_bytes);
+  if (owned) {
+    cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
+  } else {
+    ws = arena;
+  }
   char* wsa = static_cast<char*>(ws);
   cudaError_t err = flag_bytes > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
   cuda_check(err, "stream-K flags");
@@ -507,7 +539,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
       }
     }
   }
-  const cudaError_t ferr = cudaFreeAsync(ws, st);
+  const cudaError_t ferr = owned ? cudaFreeAsync(ws, st) : cudaSuccess;
   cuda_check(err, "gemm kernels");
   cuda_check(ferr, "workspace release");
   if (fc) fc->add(reference_flops(p));

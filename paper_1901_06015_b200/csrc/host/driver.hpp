@@ -43,7 +43,13 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
 // calls of the same batch may run concurrently on the device, so the kernel
 // keeps the hardware-scheduled classic grid (whose waves interleave with the
 // neighbours') instead of a stream-K tail sized for an idle GPU.
-void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared);
+// `arena` (optional): device workspace of `arena_bytes` the call may use in
+// stream order instead of allocating (gemm_batch keeps one per compute
+// stream).  `ws_needed` (optional): only report the workspace bytes the call
+// would use, launching nothing.
+void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared,
+                       void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr);
+size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared);
 
 // The value the reference's FlopCounter reaches for this plan.
 uint64_t reference_flops(const ExecutionPlan& p);

@@ -89,6 +89,44 @@ cudaEvent_t new_event() {
   return e;
 }
 
+// Grow the device's stream-ordered pool ONCE, up front, to what the batch
+// can hold at a time: one workspace arena per concurrent stream plus the
+// host staging windows in flight.  Growing it inside the batch maps memory
+// while calls are being enqueued, which stalled whole steps of the cfg2
+// sweep by 200-350 ms (measured).
+void reserve_for_batch(const std::vector<GemmCall>& calls, size_t arena_bytes, int nstreams) {
+  size_t stage = 0;
+  for (const GemmCall& g : calls) {
+    size_t st = 0;
+    for (const MatrixView* v : {&g.a, &g.b, &g.c}) {
+      const auto [lo, hi] = byte_range(*v);
+      if (hi > lo && !is_device_ptr(lo)) st += static_cast<size_t>(hi - lo);
+    }
+    stage = std::max(stage, st);
+  }
+  const size_t want = arena_bytes * static_cast<size_t>(nstreams) + stage * (kDepth + 1);
+  int dev = 0;
+  if (want == 0 || cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  uint64_t keep = ~0ULL;  // the pool must keep what is reserved (driver.cpp sets the same)
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  static std::mutex mu;
+  static std::vector<size_t> reserved;
+  std::lock_guard<std::mutex> lock(mu);
+  if (reserved.size() <= static_cast<size_t>(dev)) reserved.resize(dev + 1, 0);
+  if (want <= reserved[dev]) return;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+  const size_t bytes = std::min(want, free_b / 2);  // never take more than half of what is free
+  void* ptr = nullptr;
+  if (bytes > reserved[dev] && cudaMallocAsync(&ptr, bytes, cudaStreamLegacy) == cudaSuccess) {
+    cudaFreeAsync(ptr, cudaStreamLegacy);  // the pool keeps it (release threshold: never)
+    reserved[dev] = bytes;
+  }
+  cudaGetLastError();
+}
+
 void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc) {
   // Every plan first: policy and shape errors surface before any device work.
   std::vector<Call> cs(calls.size());
@@ -98,6 +136,20 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     cs[i].plan = plan(g.alpha, g.a, g.b, g.beta, g.c, cfg);
   }
   const Streams S = device_streams();
+  static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..8 concurrent compute streams
+    const char* f = std::getenv("MDGEMM_STREAMS");
+    const int v = f ? std::atoi(f) : 4;  // default four concurrent streams
+    return v < 1 ? 1 : (v > kComputeStreams ? kComputeStreams : v);
+  }();
+  // Workspaces (packed operands, stream-K / split-K partials): one arena per
+  // compute stream, reused by that stream's calls in stream order, sized for
+  // the largest call, instead of a pool allocation per call.
+  const bool shared = cs.size() > 1;
+  size_t arena_want = 0;
+  for (const Call& c : cs) arena_want = std::max(arena_want, workspace_bytes(c.plan, cfg.numerics, shared));
+  reserve_for_batch(calls, arena_want, std::min<int>(nstreams, static_cast<int>(cs.size())));
+  void* arena[kComputeStreams] = {};
+  size_t arena_size[kComputeStreams] = {};
   // fork from the caller's stream
   cudaEvent_t fork = new_event();
   cuda_check(cudaEventRecord(fork, user), "event");
@@ -111,6 +163,8 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
       for (cudaStream_t c : S.compute) cudaStreamSynchronize(c);
       cudaStreamSynchronize(S.out);
     }
+    for (int s = 0; s < kComputeStreams; ++s)
+      if (arena[s]) cudaFree(arena[s]);
     for (Call& c : cs) {
       for (void* q : c.buffers) cudaFree(q);
       c.buffers.clear();
@@ -123,11 +177,6 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     size_t staged = 0;  // host-staged calls issued so far (for the in-flight throttle)
     std::vector<size_t> staged_ids;
     int rr = 0;
-    static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..4 concurrent compute streams
-      const char* f = std::getenv("MDGEMM_STREAMS");
-      const int v = f ? std::atoi(f) : 4;  // default four concurrent streams
-      return v < 1 ? 1 : (v > kComputeStreams ? kComputeStreams : v);
-    }();
     double queued[kComputeStreams] = {};  // estimated work placed on each compute stream
     for (size_t i = 0; i < calls.size(); ++i) {
       Call& c = cs[i];
@@ -227,7 +276,20 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
         if (s != c.stream && latest[s] >= 0)
           cuda_check(cudaStreamWaitEvent(cst, cs[static_cast<size_t>(latest[s])].comp_done, 0), "dependency");
 
-      execute_scheduled(p, cfg.numerics, cst, fc, cs.size() > 1);
+      // (the planning-time size saw host operand addresses; a staged call's
+      // tensor-map alignment can differ, so re-check and grow in stream order)
+      const size_t ws_need = c.active ? workspace_bytes(p, cfg.numerics, shared) : 0;
+      if (ws_need > arena_size[c.stream]) {
+        if (arena[c.stream]) {
+          cuda_check(cudaFreeAsync(arena[c.stream], cst), "workspace release");
+          arena[c.stream] = nullptr;
+          arena_size[c.stream] = 0;
+        }
+        const size_t bytes = std::max(ws_need, arena_want);
+        cuda_check(cudaMallocAsync(&arena[c.stream], bytes, cst), "workspace allocation");
+        arena_size[c.stream] = bytes;
+      }
+      execute_scheduled(p, cfg.numerics, cst, fc, shared, arena[c.stream], arena_size[c.stream]);
       cuda_check(cudaEventRecord(c.comp_done, cst), "event");
 
       // ---- copy-out of a host C, release of staging
@@ -246,6 +308,12 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
         cuda_check(cudaEventRecord(c.out_done, cst), "event");
       }
     }
+    // the arenas go back to the pool after each stream's last call
+    for (int s = 0; s < kComputeStreams; ++s)
+      if (arena[s]) {
+        cuda_check(cudaFreeAsync(arena[s], S.compute[s]), "workspace release");
+        arena[s] = nullptr;
+      }
     // join back into the caller's stream
     for (const Call& c : cs) cuda_check(cudaStreamWaitEvent(user, c.out_done, 0), "join");
     if (sync) cuda_check(cudaStreamSynchronize(user), "gemm synchronisation");
