@@ -268,10 +268,12 @@ ExecutionPlan plan(Scalar alpha, const MatrixView& a, const MatrixView& b, Scala
 void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta,
           const MatrixView& c, const Config& cfg = Config::defaults(), FlopCounter* fc = nullptr);
 
-// A list of independent gemm() calls, equivalent to calling gemm() on each in
-// order, with the host-operand staging of one call overlapped with the
-// kernels of its neighbours (copy-in / compute / copy-out streams).
-// Synchronous.  B200 extension.
+// A list of gemm() calls, equivalent to calling gemm() on each in order.
+// Host operand windows are copied into HBM once per batch and stay resident
+// (calls sharing an operand reuse the device copy; a host C goes back once,
+// after its last writer); copies overlap the kernels of neighbouring calls,
+// and calls touching disjoint memory run concurrently.  Synchronous.  B200
+// extension.
 struct GemmCall {
   Scalar alpha;
   MatrixView a, b;
@@ -284,6 +286,10 @@ void gemm_batch(const std::vector<GemmCall>& calls, const Config& cfg = Config::
 // synchronising; host operands must stay valid until the stream completes.
 void gemm_batch_async(const std::vector<GemmCall>& calls, const Config& cfg, void* stream,
                       FlopCounter* fc = nullptr);
+
+// Bytes the batch runner has copied host->device and device->host so far
+// (process-wide counters).
+void staging_bytes(uint64_t* h2d, uint64_t* d2h);
 
 // Device-pointer variant ordered on `stream` (a cudaStream_t); returns
 // without synchronising.

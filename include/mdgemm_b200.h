@@ -170,9 +170,11 @@ int mdg_gemm(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b,
              mdg_scalar_t beta, const mdg_view_t* c, const mdg_config_t* cfg,
              uint64_t* flops_out);
 
-/* A batch of independent gemm() calls, equivalent to mdg_gemm on each in
- * order; host operands are staged with copy-in / compute / copy-out
- * pipelined across calls.  Synchronous. */
+/* A batch of gemm() calls, equivalent to mdg_gemm on each in order.  Each
+ * distinct host operand window crosses PCIe once per batch (it stays
+ * resident in HBM while later calls read or update it; a host C is copied
+ * back once, after its last writer); copies overlap neighbouring calls'
+ * kernels and calls touching disjoint memory run concurrently.  Synchronous. */
 typedef struct mdg_gemm_call {
   mdg_scalar_t alpha;
   mdg_view_t a, b;
@@ -238,6 +240,8 @@ typedef struct mdg_kernel_stats {
 } mdg_kernel_stats_t;
 
 uint64_t mdg_launch_count(void);
+/* Bytes the batch runner has staged host->device / device->host so far. */
+void mdg_staging_bytes(uint64_t* h2d, uint64_t* d2h);
 int mdg_profile_begin(void);
 int mdg_profile_end(mdg_kernel_stats_t* out /* [MDG_KERNEL_KINDS] */);
 

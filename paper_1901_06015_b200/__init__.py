@@ -258,6 +258,7 @@ def _load() -> ctypes.CDLL:
         "mdg_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
         "mdg_shard_columns": (c_int, [c_int64, c_int32, c_int32, c_int64, POINTER(c_int64), POINTER(c_int64)]),
         "mdg_launch_count": (c_uint64, []),
+        "mdg_staging_bytes": (None, [POINTER(c_uint64), POINTER(c_uint64)]),
         "mdg_profile_begin": (c_int, []),
         "mdg_profile_end": (c_int, [POINTER(KernelStats)]),
     }
@@ -274,13 +275,20 @@ EXPORTED_SYMBOLS = (
     "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_batch_async", "mdg_gemm_async",
     "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
-    "mdg_launch_count", "mdg_profile_begin", "mdg_profile_end",
+    "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
 )
 
 
 def launch_count() -> int:
     """Kernels this process has launched through the library."""
     return lib.mdg_launch_count()
+
+
+def staging_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes the batch runner has copied so far."""
+    h2d, d2h = c_uint64(0), c_uint64(0)
+    lib.mdg_staging_bytes(byref(h2d), byref(d2h))
+    return h2d.value, d2h.value
 
 
 def profile_begin() -> None:

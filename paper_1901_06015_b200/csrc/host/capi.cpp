@@ -367,6 +367,8 @@ int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align, int
 
 uint64_t mdg_launch_count(void) { return prof::launches(); }
 
+void mdg_staging_bytes(uint64_t* h2d, uint64_t* d2h) { mdgemm::staging_bytes(h2d, d2h); }
+
 int mdg_profile_begin(void) {
   return guarded([&] { prof::begin(); });
 }

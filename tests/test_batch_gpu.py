@@ -104,3 +104,85 @@ def test_batch_errors_before_device_work():
     with pytest.raises(M.ScalarPolicyError):
         M.gemm_batch([(SCALARS["one"], qa, qb, SCALARS["one"], qc), (SCALARS["c55"], pa, pb, SCALARS["one"], pc)])
     assert np.array_equal(before, q.C.buf)  # the valid first call did not run either
+
+
+def _sub(buf: np.ndarray, dtype: int, ld: int, i0: int, j0: int, m: int, n: int, comp=None):
+    """Column-major sub-view of a host buffer with leading dimension ld."""
+    es = M.dtype_size(dtype)
+    v = M.MatrixView.make(buf.ctypes.data + (i0 + j0 * ld) * es, m, n, 1, ld, dtype)
+    return v.with_comp_prec(comp) if comp is not None else v
+
+
+def _sequential_exact(seq, bufs, cfg):
+    """Run (alpha, a, b, beta, c) recipes one after another with the oracle on copies of bufs."""
+    ref = {k: b.copy() for k, b in bufs.items()}
+    for alpha, a, b, beta, c in seq:
+        O.orc_gemm(alpha, a(ref), b(ref), beta, c(ref), cfg)
+    return ref
+
+
+def test_batch_shared_host_operands_cross_pcie_once():
+    """Every distinct host window is copied in once per batch and a host C goes back once."""
+    cfg = config({"gpu.numerics": "exact"})
+    A = HostMatrix(M.DT_Z, 48, 40).fill(O.orc_rng_state(1, ["a"]))
+    B = HostMatrix(M.DT_D, 40, 36).fill(O.orc_rng_state(1, ["b"]))
+    C = HostMatrix(M.DT_Z, 48, 36).fill(O.orc_rng_state(1, ["c"]))
+    want = C.clone()
+    for _ in range(5):
+        O.orc_gemm(SCALARS["p7"], A.view(), B.view(), SCALARS["cfg2_beta"], want.view(), cfg)
+    h0, d0 = M.staging_bytes()
+    M.gemm_batch([(SCALARS["p7"], A.view(), B.view(), SCALARS["cfg2_beta"], C.view())] * 5, cfg)
+    h1, d1 = M.staging_bytes()
+    assert C.buf.tobytes() == want.buf.tobytes()
+    assert h1 - h0 == A.buf.nbytes + B.buf.nbytes + C.buf.nbytes
+    assert d1 - d0 == C.buf.nbytes
+
+
+@pytest.mark.parametrize("budget_mb", [None, "0.02"])
+def test_batch_overlapping_host_windows(monkeypatch, budget_mb):
+    """Host operands that are sub-views of one buffer, overlapping each other and earlier residents
+    (straddling, containing, contained), with and without forced evictions: the batch equals
+    sequential gemm() calls bitwise (EXACT numerics)."""
+    if budget_mb:
+        monkeypatch.setenv("MDGEMM_RESIDENT_MB", budget_mb)
+    cfg = config({"gpu.numerics": "exact"})
+    ld = 64
+    X = HostMatrix(M.DT_D, ld, 96).fill(O.orc_rng_state(2, ["x"]))
+    Y = HostMatrix(M.DT_D, ld, 96).fill(O.orc_rng_state(2, ["y"]))
+    Z = HostMatrix(M.DT_D, ld, 96).fill(O.orc_rng_state(2, ["z"]))
+    bufs = {"X": X.buf, "Y": Y.buf, "Z": Z.buf}
+    D = M.DT_D
+
+    def sv(name, i0, j0, m, n):
+        return lambda b: _sub(b[name], D, ld, i0, j0, m, n)
+    seq = [
+        (SCALARS["one"], sv("X", 0, 0, 32, 16), sv("Y", 0, 0, 16, 24), SCALARS["one"], sv("Y", 0, 40, 32, 24)),
+        # A straddles the C window of call 0 (columns 30..50 of Y)
+        (SCALARS["one"], sv("Y", 3, 30, 32, 20), sv("X", 0, 20, 20, 24), SCALARS["p3"], sv("X", 0, 60, 32, 24)),
+        # A and B overlap each other inside one call
+        (SCALARS["p7"], sv("X", 0, 10, 24, 30), sv("X", 5, 20, 30, 16), SCALARS["m3"], sv("Y", 8, 70, 24, 16)),
+        # B contains everything written so far in Y
+        (SCALARS["one"], sv("X", 0, 0, 40, 64), sv("Y", 0, 0, 64, 90), SCALARS["one"], sv("Z", 20, 0, 40, 90)),
+        # C inside an earlier (read) window
+        (SCALARS["one"], sv("Y", 0, 0, 16, 8), sv("Y", 16, 8, 8, 12), SCALARS["p3"], sv("X", 2, 2, 16, 12)),
+    ]
+    ref = _sequential_exact(seq, bufs, cfg)
+    M.gemm_batch([(al, a(bufs), b(bufs), be, c(bufs)) for al, a, b, be, c in seq], cfg)
+    for k in bufs:
+        assert bufs[k].tobytes() == ref[k].tobytes(), k
+
+
+def test_batch_eviction_chain(monkeypatch):
+    """A dependency chain over more host data than the resident budget: evicted results go back to
+    the host and are re-read correctly."""
+    monkeypatch.setenv("MDGEMM_RESIDENT_MB", "0.1")
+    cfg = config({"gpu.numerics": "fast"})
+    mats = [HostMatrix(M.DT_D, 64, 64).fill(O.orc_rng_state(4, [str(i)])) for i in range(8)]
+    ref = [m.clone() for m in mats]
+    seq = [(i % 8, (i + 3) % 8, (i + 5) % 8) for i in range(20)]
+    for a, b, c in seq:
+        M.gemm(SCALARS["p7"], ref[a].view(), ref[b].view(), SCALARS["m3"], ref[c].view(), cfg)
+    M.gemm_batch([(SCALARS["p7"], mats[a].view(), mats[b].view(), SCALARS["m3"], mats[c].view()) for a, b, c in seq],
+                 cfg)
+    for i in range(8):
+        assert mats[i].buf.tobytes() == ref[i].buf.tobytes(), i
