@@ -230,7 +230,11 @@ int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align,
  * pack / beta kernels). */
 enum {
   MDG_KERNEL_PACK = 0, MDG_KERNEL_DMMA = 1, MDG_KERNEL_FFMA = 2, MDG_KERNEL_EXACT = 3,
-  MDG_KERNEL_BETA = 4, MDG_KERNEL_FILL = 5, MDG_KERNEL_KINDS = 6
+  MDG_KERNEL_BETA = 4, MDG_KERNEL_FILL = 5,
+  /* the dual-pipe kernel (gemm_batch): each launch is recorded under both
+   * kinds with the same device time, its work split by pipe (FP64 DMMA flops
+   * under DUAL_D, FP32 FFMA flops under DUAL_F; DUAL_F counts no launch) */
+  MDG_KERNEL_DUAL_D = 6, MDG_KERNEL_DUAL_F = 7, MDG_KERNEL_KINDS = 8
 };
 
 typedef struct mdg_kernel_stats {

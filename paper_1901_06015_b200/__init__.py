@@ -216,7 +216,7 @@ class KernelStats(ctypes.Structure):
     _fields_ = [("launches", c_uint64), ("total_ms", c_double), ("work", c_double)]
 
 
-KERNEL_KINDS = ("pack", "dmma", "ffma", "exact", "beta", "fill")
+KERNEL_KINDS = ("pack", "dmma", "ffma", "exact", "beta", "fill", "dual_d", "dual_f")
 
 
 def _round(v: float, prec: int) -> float:

@@ -120,6 +120,33 @@ inline __host__ __device__ int64_t sk_launch_grid(int64_t tiles, int64_t G) {
 // Word 5: the producer's first bulk-copy issue.
 constexpr int TRACE_WORDS = 6;
 
+// One job of the dual-pipe kernel (gemm_dual.cu): a FAST gemm whose operands
+// are already packed with the group's tile as panel dimension (D group:
+// 128-row A panels, 128-column B panels, doubles; F group: 64 / 128, floats)
+// and panel length lpad (a multiple of 16).
+struct DualJob {
+  const void* a;
+  const void* b;
+  int64_t lpad;
+  int64_t me, ne;
+  DView out;
+  DBeta beta;
+  int32_t pair;
+  int32_t tiles_m, tiles_n;
+  int32_t tile0;  // first virtual tile of the job in its group's list
+};
+constexpr int DUAL_MAX_JOBS = 80;  // per group and launch (kernel parameter space)
+struct DualDesc {
+  int32_t nd, nf;            // jobs per group
+  int32_t tiles_d, tiles_f;  // virtual tiles per group
+  int32_t prefetch_c;        // producers warm L2 with each tile's C
+  int32_t pad0;
+  unsigned long long* timing;  // tuning only: {start min, D end max, F end max} (%globaltimer ns) or null
+  DualJob d[DUAL_MAX_JOBS];
+  DualJob f[DUAL_MAX_JOBS];
+};
+constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128, DUAL_BK = 16;
+
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);
 cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s);
@@ -144,6 +171,9 @@ cudaError_t launch_gemm_ffma_ws(const GemmDesc& d, int grid, cudaStream_t s);
 // (occupancy query; sizes the split-K and stream-K grids).
 int dmma_ctas_per_sm(const FastTile& t, int cdt);
 int ffma_ctas_per_sm(const FastTile& t, int cdt);
+// Dual-pipe kernel: one CTA per SM (grid), D and F groups on their job lists.
+size_t dual_smem();
+cudaError_t launch_gemm_dual(const DualDesc& d, int grid, cudaStream_t s);
 // Split-K: sum the `splits` partial tiles in split order and run the fused
 // epilogue (one CTA per tile).
 cudaError_t launch_splitk_reduce(const GemmDesc& d, const FastTile& t, bool single, cudaStream_t s);

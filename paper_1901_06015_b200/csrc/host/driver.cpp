@@ -545,4 +545,69 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   if (fc) fc->add(reference_flops(p));
 }
 
+// ---------------------------------------------------------------- dual-pipe jobs
+bool dual_eligible(const ExecutionPlan& p, Numerics numerics) {
+  if (numerics != Numerics::Fast || p.m <= 0 || p.n <= 0 || p.k <= 0) return false;
+  if (p.c.dtype.domain == Domain::Complex && p.pair_axis == PairAxis::None) return false;
+  const int64_t bm = p.comp_prec == Precision::Single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
+  const int64_t tiles = ((p.m + bm - 1) / bm) * ((p.n + mdg::DUAL_D_BN - 1) / mdg::DUAL_D_BN);
+  return tiles < (int64_t{1} << 30);
+}
+
+DualPrep dual_prepare(const ExecutionPlan& p) {
+  DualPrep d;
+  d.single = p.comp_prec == Precision::Single;
+  const int64_t bm = d.single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
+  const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
+  d.lpad = (p.k + mdg::DUAL_BK - 1) / mdg::DUAL_BK * mdg::DUAL_BK;
+  const Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, bm, d.lpad);
+  const Packed pb = prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, bn, d.lpad);
+  d.pa = pa.desc;
+  d.pb = pb.desc;
+  d.bytes_a = pa.bytes;
+  d.bytes_b = pb.bytes;
+  d.off_b = (pa.bytes + 255) / 256 * 256;
+  d.bytes = d.off_b + (pb.bytes + 255) / 256 * 256;
+  d.tile_flops = 2.0 * static_cast<double>((p.m + bm - 1) / bm * bm) * static_cast<double>((p.n + bn - 1) / bn * bn) *
+                 static_cast<double>(d.lpad);
+  return d;
+}
+
+void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job) {
+  const DualPrep d = dual_prepare(p);
+  char* w = static_cast<char*>(ws);
+  {
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a));
+    cuda_check(mdg::launch_pack(d.pa, w, st), "pack kernel");
+  }
+  {
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, d.bytes_b));
+    cuda_check(mdg::launch_pack(d.pb, w + d.off_b, st), "pack kernel");
+  }
+  const int64_t bm = d.single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
+  const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
+  *job = mdg::DualJob{};
+  job->a = w;
+  job->b = w + d.off_b;
+  job->lpad = d.lpad;
+  job->me = p.m;
+  job->ne = p.n;
+  job->out = to_dview(p.c);
+  job->beta = to_dbeta(p.beta);
+  job->pair = static_cast<int32_t>(p.pair_axis);
+  job->tiles_m = static_cast<int32_t>((p.m + bm - 1) / bm);
+  job->tiles_n = static_cast<int32_t>((p.n + bn - 1) / bn);
+}
+
+void dual_launch(const mdg::DualDesc& desc, double flops_d, double flops_f, cudaStream_t st) {
+  mdg::DualDesc& d = const_cast<mdg::DualDesc&>(desc);
+  static const int prefetch = [] {  // tuning: MDGEMM_DUAL_PREFETCH = 0 turns the C L2 prefetch off
+    const char* f = std::getenv("MDGEMM_DUAL_PREFETCH");
+    return f ? std::atoi(f) : 1;
+  }();
+  d.prefetch_c = prefetch;
+  prof::Scope scope(MDG_KERNEL_DUAL_D, st, flops_d, MDG_KERNEL_DUAL_F, flops_f);
+  cuda_check(mdg::launch_gemm_dual(d, device_sms(), st), "dual-pipe gemm kernel");
+}
+
 }  // namespace mdgemm

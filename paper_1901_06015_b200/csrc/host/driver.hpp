@@ -51,6 +51,27 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, 
                        void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr);
 size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared);
 
+// ---- the dual-pipe kernel (gemm_dual.cu), used by gemm_batch -------------
+// FAST plans it can run: k > 0, non-empty, complex C paired.
+bool dual_eligible(const ExecutionPlan& p, Numerics numerics);
+// Packed operands of a dual job: A panels of the group's tile rows, B panels
+// of its tile columns, k padded to 16; `bytes` of workspace, B at `off_b`.
+struct DualPrep {
+  mdg::PackDesc pa{}, pb{};
+  size_t bytes_a = 0, bytes_b = 0;
+  size_t off_b = 0, bytes = 0;
+  int64_t lpad = 0;
+  bool single = false;
+  double tile_flops = 0.0;  // flops of the padded tile grid (2 tiles*BM*BN*lpad)
+};
+DualPrep dual_prepare(const ExecutionPlan& p);
+// Launch the two pack kernels into ws (stream-ordered) and describe the job
+// (p's views must be the device views the kernels read).
+void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job);
+// One dual launch over d's job lists (grid = SMs); flops per group for the
+// profiling hook.
+void dual_launch(const mdg::DualDesc& d, double flops_d, double flops_f, cudaStream_t st);
+
 // The value the reference's FlopCounter reaches for this plan.
 uint64_t reference_flops(const ExecutionPlan& p);
 

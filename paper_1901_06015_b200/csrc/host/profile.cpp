@@ -16,6 +16,8 @@ struct Record {
   int kind;
   cudaEvent_t start, stop;
   double work;
+  int kind2;
+  double work2;
 };
 
 struct ThreadLog {
@@ -46,11 +48,16 @@ Scope::Scope(int kind, cudaStream_t stream, double work) : kind_(kind), stream_(
   cudaEventRecord(start_, stream_);
 }
 
+Scope::Scope(int kind, cudaStream_t stream, double work, int kind2, double work2) : Scope(kind, stream, work) {
+  kind2_ = kind2;
+  work2_ = work2;
+}
+
 Scope::~Scope() {
   if (!start_) return;
   cudaEvent_t stop = g_log.take();
   cudaEventRecord(stop, stream_);
-  g_log.records.push_back(Record{kind_, start_, stop, work_});
+  g_log.records.push_back(Record{kind_, start_, stop, work_, kind2_, work2_});
 }
 
 uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
@@ -70,6 +77,10 @@ void end(mdg_kernel_stats_t* out) {
     s.launches += 1;
     s.total_ms += ms;
     s.work += r.work;
+    if (r.kind2 >= 0) {
+      out[r.kind2].total_ms += ms;
+      out[r.kind2].work += r.work2;
+    }
     g_log.spare.push_back(r.start);
     g_log.spare.push_back(r.stop);
   }

@@ -13,6 +13,8 @@ namespace mdgemm::prof {
 class Scope {
  public:
   Scope(int kind, cudaStream_t stream, double work);
+  // one launch whose time also counts under kind2 with work2 (no extra launch)
+  Scope(int kind, cudaStream_t stream, double work, int kind2, double work2);
   ~Scope();
   Scope(const Scope&) = delete;
   Scope& operator=(const Scope&) = delete;
@@ -21,6 +23,8 @@ class Scope {
   int kind_;
   cudaStream_t stream_;
   double work_;
+  int kind2_ = -1;
+  double work2_ = 0.0;
   cudaEvent_t start_ = nullptr;
 };
 

@@ -21,6 +21,7 @@
 // copy) overlaps its reads or writes, or vice versa.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -167,6 +168,434 @@ size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
   return budget;
 }
 
+// ------------------------------------------------------------- dual-pipe mode
+// A batch whose calls include both computation precisions runs on the
+// dual-pipe kernel (gemm_dual.cu): calls are list-scheduled into launches,
+// each pairing FP64 (DMMA) jobs with FP32 (FFMA2) jobs whose estimated
+// durations match, so both pipes of every SM work at once.  A launch holds
+// only calls whose dependencies (device-memory conflicts, as in the stream
+// scheduler) completed in earlier launches; launches run in order on one
+// stream, their packs on a second stream into two alternating arenas (the
+// packs of launch u+1 fill SMs freed by the tail of launch u).  Calls the
+// kernel does not take (EXACT numerics, k = 0, ...) run in the same order
+// through execute().  Host operands are staged once up front (only when no
+// two host windows of the batch partially overlap and they fit the resident
+// budget; otherwise the batch takes the stream scheduler below).
+namespace {
+
+// device rates of the two groups while both run, measured per launch on the
+// cfg2 sweep (MDGEMM_DUAL_LOG: group end times): 27.3 + 29.6 TFLOP/s
+// (tools/dual_probe's register-light loops: 28.7 + 34.9)
+constexpr double kDualRateD = 27.3e12, kDualRateF = 29.6e12;
+
+struct Unit {
+  std::vector<size_t> d, f;  // dual jobs (call indices)
+  long classic = -1;         // or one call through execute()
+  size_t bytes = 0;          // packed operand bytes of the dual jobs
+};
+
+int dual_mode() {
+  const char* f = std::getenv("MDGEMM_DUAL");  // 0 off, 1 auto, 2 force (even one-precision batches)
+  return f ? std::atoi(f) : 1;
+}
+
+}  // namespace
+
+bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
+                  cudaStream_t user, bool sync, FlopCounter* fc) {
+  const int mode = dual_mode();
+  const size_t n = cs.size();
+  if (mode == 0 || n < 2 || cfg.numerics != Numerics::Fast) return false;
+  std::vector<int> kind(n, 0);  // 0 classic, 1 D, 2 F
+  size_t nd = 0, nf = 0;
+  for (size_t i = 0; i < n; ++i)
+    if (dual_eligible(cs[i].plan, cfg.numerics)) {
+      kind[i] = cs[i].plan.comp_prec == Precision::Single ? 2 : 1;
+      (kind[i] == 1 ? nd : nf) += 1;
+    }
+  if (mode == 1 && (nd == 0 || nf == 0)) return false;
+  if (nd + nf == 0) return false;
+
+  // ---- host windows: per-call hulls; any two overlapping hulls must be identical
+  std::vector<std::vector<Window>> hulls(n);
+  std::vector<Window> all;
+  for (size_t i = 0; i < n; ++i) {
+    std::vector<Window>& hs = hulls[i];
+    for (int r = 0; r < 3; ++r)
+      if (cs[i].host[r]) hs.push_back(cs[i].win[r]);
+    for (bool changed = true; changed;) {
+      changed = false;
+      for (size_t x = 0; x < hs.size() && !changed; ++x)
+        for (size_t y = x + 1; y < hs.size() && !changed; ++y)
+          if (hs[x].overlaps(hs[y])) {
+            hs[x] = Window{std::min(hs[x].lo, hs[y].lo), std::max(hs[x].hi, hs[y].hi)};
+            hs.erase(hs.begin() + static_cast<long>(y));
+            changed = true;
+          }
+    }
+    all.insert(all.end(), hs.begin(), hs.end());
+  }
+  std::sort(all.begin(), all.end(), [](const Window& a, const Window& b) {
+    return a.lo != b.lo ? a.lo < b.lo : a.hi < b.hi;
+  });
+  all.erase(std::unique(all.begin(), all.end(), [](const Window& a, const Window& b) { return a.lo == b.lo && a.hi == b.hi; }),
+            all.end());
+  size_t host_bytes = 0;
+  for (size_t x = 0; x < all.size(); ++x) {
+    host_bytes += all[x].bytes();
+    if (x + 1 < all.size() && all[x].overlaps(all[x + 1])) return false;
+  }
+
+  // ---- device windows (host operands at their future resident copies) and dependencies
+  // Residents are laid out later; for conflict analysis a host window stands for itself
+  // (host and device address ranges never mix within one window).
+  for (size_t i = 0; i < n; ++i) {
+    Call& c = cs[i];
+    for (int r = 0; r < 3; ++r) {
+      if (c.win[r].empty()) continue;
+      if (r < 2) c.dev_read[r] = c.win[r];
+      else c.dev_write = c.win[r];
+    }
+  }
+  struct WinState {
+    Window w;
+    long writer = -1;
+    std::vector<long> readers;
+  };
+  std::vector<WinState> ws;
+  std::vector<std::vector<long>> succ(n);
+  std::vector<int> npred(n, 0);
+  std::vector<long> ab_writer(n, -1);  // latest call writing what this call's A/B read (packs wait for it)
+  for (size_t i = 0; i < n; ++i) {
+    const Call& c = cs[i];
+    std::vector<long> preds;
+    for (const WinState& w : ws) {
+      for (int r = 0; r < 2; ++r)
+        if (w.writer >= 0 && w.w.overlaps(c.dev_read[r])) {
+          preds.push_back(w.writer);
+          ab_writer[i] = std::max(ab_writer[i], w.writer);
+        }
+      if (w.w.overlaps(c.dev_write)) {
+        if (w.writer >= 0) preds.push_back(w.writer);
+        preds.insert(preds.end(), w.readers.begin(), w.readers.end());
+      }
+    }
+    std::sort(preds.begin(), preds.end());
+    preds.erase(std::unique(preds.begin(), preds.end()), preds.end());
+    for (long h : preds) succ[static_cast<size_t>(h)].push_back(static_cast<long>(i));
+    npred[i] = static_cast<int>(preds.size());
+    auto find = [&](const Window& x) -> WinState& {
+      for (WinState& w : ws)
+        if (w.w.lo == x.lo && w.w.hi == x.hi) return w;
+      ws.push_back(WinState{x, -1, {}});
+      return ws.back();
+    };
+    for (int r = 0; r < 2; ++r)
+      if (!c.dev_read[r].empty()) find(c.dev_read[r]).readers.push_back(static_cast<long>(i));
+    if (!c.dev_write.empty()) {
+      for (WinState& w : ws)
+        if (w.w.overlaps(c.dev_write)) {
+          w.writer = static_cast<long>(i);
+          w.readers.clear();
+        }
+      WinState& mine = find(c.dev_write);
+      mine.writer = static_cast<long>(i);
+      mine.readers.clear();
+    }
+  }
+
+  // ---- list schedule
+  std::vector<DualPrep> prep(n);
+  std::vector<double> est(n, 0.0);
+  size_t max_call_bytes = 0;
+  for (size_t i = 0; i < n; ++i)
+    if (kind[i]) {
+      prep[i] = dual_prepare(cs[i].plan);
+      est[i] = prep[i].tile_flops / (kind[i] == 1 ? kDualRateD : kDualRateF);
+      max_call_bytes = std::max(max_call_bytes, prep[i].bytes);
+    }
+  const size_t unit_cap = std::max(max_call_bytes, size_t{6} << 30);  // packed bytes per launch
+  // priority: the longest remaining dependency path (critical path first), so
+  // long chains advance early and the last launches still pair both pipes
+  std::vector<double> tail(n, 0.0);
+  for (size_t i = n; i-- > 0;) {
+    double t = 0.0;
+    for (long s2 : succ[i]) t = std::max(t, tail[static_cast<size_t>(s2)]);
+    tail[i] = t + (kind[i] ? est[i] : 1e-5);
+  }
+  auto by_priority = [&](size_t x, size_t y) { return tail[x] != tail[y] ? tail[x] > tail[y] : x < y; };
+  std::vector<Unit> units;
+  std::vector<long> unit_of(n, -1);
+  std::vector<size_t> ready;
+  for (size_t i = 0; i < n; ++i)
+    if (npred[i] == 0) ready.push_back(i);
+  std::sort(ready.begin(), ready.end(), by_priority);
+  size_t done = 0;
+  while (done < n) {
+    Unit u;
+    auto it = std::find_if(ready.begin(), ready.end(), [&](size_t i) { return kind[i] == 0; });
+    if (it != ready.end()) {
+      u.classic = static_cast<long>(*it);
+    } else {
+      double td = 0, tf = 0;
+      for (size_t i : ready) (kind[i] == 1 ? td : tf) += est[i];
+      const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? td / 2 : td);
+      const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? tf / 2 : tf);
+      // in priority order, jobs that keep each side within 5 % of its target;
+      // then, if a side fell short, its best remaining job (one overshoot)
+      double ad = 0, af = 0;
+      auto fits = [&](size_t i, bool loose) {
+        const bool isd = kind[i] == 1;
+        const std::vector<size_t>& lst = isd ? u.d : u.f;
+        const double acc = isd ? ad : af, target = isd ? target_d : target_f;
+        if (lst.size() >= static_cast<size_t>(mdg::DUAL_MAX_JOBS)) return false;
+        if (!(u.d.empty() && u.f.empty()) && u.bytes + prep[i].bytes > unit_cap) return false;
+        if (lst.empty()) return true;
+        return loose ? acc < target * 0.95 : acc + est[i] <= target * 1.05;
+      };
+      auto take = [&](size_t i) {
+        (kind[i] == 1 ? u.d : u.f).push_back(i);
+        (kind[i] == 1 ? ad : af) += est[i];
+        u.bytes += prep[i].bytes;
+      };
+      std::vector<char> used(ready.size(), 0);
+      for (int pass = 0; pass < 2; ++pass)
+        for (size_t x = 0; x < ready.size(); ++x)
+          if (!used[x] && fits(ready[x], pass == 1)) {
+            take(ready[x]);
+            used[x] = 1;
+          }
+    }
+    const long uid = static_cast<long>(units.size());
+    std::vector<size_t> members = u.d;
+    members.insert(members.end(), u.f.begin(), u.f.end());
+    if (u.classic >= 0) members.push_back(static_cast<size_t>(u.classic));
+    for (size_t i : members) {
+      unit_of[i] = uid;
+      ready.erase(std::find(ready.begin(), ready.end(), i));
+    }
+    done += members.size();
+    std::vector<size_t> newly;
+    for (size_t i : members)
+      for (long s : succ[i])
+        if (--npred[static_cast<size_t>(s)] == 0) newly.push_back(static_cast<size_t>(s));
+    ready.insert(ready.end(), newly.begin(), newly.end());
+    std::sort(ready.begin(), ready.end(), by_priority);
+    // longest k first: the virtual tile order front-loads the longest tiles
+    auto by_k = [&](size_t x, size_t y) { return prep[x].lpad > prep[y].lpad; };
+    std::stable_sort(u.d.begin(), u.d.end(), by_k);
+    std::stable_sort(u.f.begin(), u.f.end(), by_k);
+    units.push_back(std::move(u));
+  }
+  size_t arena_bytes = 0;
+  for (const Unit& u : units) arena_bytes = std::max(arena_bytes, u.bytes);
+  if (const char* logp = std::getenv("MDGEMM_DUAL_LOG")) {  // tuning: the launch schedule
+    if (FILE* f = std::fopen(logp, "a")) {
+      std::fprintf(f, "batch %zu calls -> %zu launches\n", n, units.size());
+      for (const Unit& u : units) {
+        double td = 0, tf = 0;
+        for (size_t i : u.d) td += est[i];
+        for (size_t i : u.f) tf += est[i];
+        std::fprintf(f, "  D %2zu jobs %8.3f ms | F %2zu jobs %8.3f ms | classic %ld | %.2f GB\n", u.d.size(), td * 1e3,
+                     u.f.size(), tf * 1e3, u.classic, u.bytes / 1e9);
+      }
+      std::fclose(f);
+    }
+  }
+  const size_t budget = reserve_for_batch(host_bytes, arena_bytes, 2);
+  if (host_bytes > budget) {  // does not fit: the stream scheduler evicts as it goes
+    for (Call& c : cs) c.dev_read[0] = c.dev_read[1] = c.dev_write = Window{};
+    return false;
+  }
+
+  // ---- emission
+  cudaStream_t K = S.compute[0], P = S.compute[1];
+  std::vector<cudaEvent_t> events;
+  auto ev = [&]() {
+    events.push_back(new_event());
+    return events.back();
+  };
+  std::vector<std::pair<Window, std::byte*>> residents;  // host window -> device copy
+  void* arena[2] = {nullptr, nullptr};
+  bool failed = true;
+  auto cleanup = [&](bool wait) {
+    if (wait) {
+      cudaStreamSynchronize(S.in);
+      cudaStreamSynchronize(K);
+      cudaStreamSynchronize(P);
+      cudaStreamSynchronize(S.out);
+      for (auto& r : residents) cudaFree(r.second);
+      for (void* a : arena)
+        if (a) cudaFree(a);
+    }
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    for (Call& c : cs)
+      if (c.comp_done) cudaEventDestroy(c.comp_done);
+  };
+  try {
+    cudaEvent_t fork = ev();
+    cuda_check(cudaEventRecord(fork, user), "event");
+    for (cudaStream_t st : {S.in, K, P, S.out}) cuda_check(cudaStreamWaitEvent(st, fork, 0), "fork");
+    // host operands: one resident copy per distinct window
+    for (const Window& w : all) {
+      void* d = nullptr;
+      cuda_check(cudaMallocAsync(&d, w.bytes(), S.in), "staging allocation");
+      residents.emplace_back(w, static_cast<std::byte*>(d));
+      cuda_check(cudaMemcpyAsync(d, w.lo, w.bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
+      g_h2d_bytes.fetch_add(w.bytes(), std::memory_order_relaxed);
+    }
+    if (!all.empty()) {
+      cudaEvent_t staged = ev();
+      cuda_check(cudaEventRecord(staged, S.in), "event");
+      cuda_check(cudaStreamWaitEvent(K, staged, 0), "dependency");
+      cuda_check(cudaStreamWaitEvent(P, staged, 0), "dependency");
+    }
+    auto rebase = [&](size_t i) {
+      Call& c = cs[i];
+      ExecutionPlan& p = c.plan;
+      for (int r = 0; r < 3; ++r) {
+        if (!c.host[r]) continue;
+        std::byte* base = nullptr;
+        for (auto& rs : residents)
+          if (rs.first.contains(c.win[r])) base = rs.second + (c.win[r].lo - rs.first.lo);
+        for (MatrixView* v : {&p.a, &p.b, &p.c})
+          if (v->base >= c.win[r].lo && v->base < c.win[r].hi) v->base = base + (v->base - c.win[r].lo);
+      }
+    };
+    for (size_t i = 0; i < n; ++i) rebase(i);
+    if (arena_bytes > 0)
+      for (void*& a : arena) cuda_check(cudaMallocAsync(&a, arena_bytes, P), "workspace allocation");
+    std::vector<cudaEvent_t> k_done(units.size(), nullptr);
+    const char* log_path = std::getenv("MDGEMM_DUAL_LOG");
+    const bool log_units = log_path != nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> unit_ev(units.size(), {nullptr, nullptr});
+    unsigned long long* timing_buf = nullptr;
+    for (auto& pr : unit_ev) {
+      pr.first = nullptr;
+      pr.second = nullptr;
+    }
+    for (size_t ui = 0; ui < units.size(); ++ui) {
+      const Unit& u = units[ui];
+      if (u.classic >= 0) {
+        Call& c = cs[static_cast<size_t>(u.classic)];
+        execute_scheduled(c.plan, cfg.numerics, K, fc, true);
+      } else {
+        // packs: after the kernel that last used this arena and after writers of the A/B read
+        if (ui >= 2 && k_done[ui - 2]) cuda_check(cudaStreamWaitEvent(P, k_done[ui - 2], 0), "arena reuse");
+        long abw = -1;
+        for (const std::vector<size_t>* lst : {&u.d, &u.f})
+          for (size_t i : *lst)
+            if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
+        if (abw >= 0 && k_done[static_cast<size_t>(abw)])
+          cuda_check(cudaStreamWaitEvent(P, k_done[static_cast<size_t>(abw)], 0), "dependency");
+        mdg::DualDesc dd{};
+        double flops_d = 0, flops_f = 0;
+        char* w = static_cast<char*>(arena[ui % 2]);
+        size_t off = 0;
+        for (int grp = 0; grp < 2; ++grp) {
+          const std::vector<size_t>& lst = grp == 0 ? u.d : u.f;
+          mdg::DualJob* jobs = grp == 0 ? dd.d : dd.f;
+          int32_t tiles = 0;
+          for (size_t x = 0; x < lst.size(); ++x) {
+            const size_t i = lst[x];
+            dual_pack(cs[i].plan, w + off, P, &jobs[x]);
+            off += prep[i].bytes;
+            jobs[x].tile0 = tiles;
+            tiles += jobs[x].tiles_m * jobs[x].tiles_n;
+            const ExecutionPlan& p = cs[i].plan;
+            (grp == 0 ? flops_d : flops_f) += 2.0 * p.m * p.n * p.k;
+          }
+          (grp == 0 ? dd.nd : dd.nf) = static_cast<int32_t>(lst.size());
+          (grp == 0 ? dd.tiles_d : dd.tiles_f) = tiles;
+        }
+        cudaEvent_t packed = ev();
+        cuda_check(cudaEventRecord(packed, P), "event");
+        cuda_check(cudaStreamWaitEvent(K, packed, 0), "dependency");
+        if (log_units) {
+          if (!timing_buf) cuda_check(cudaMalloc(&timing_buf, units.size() * 3 * 8), "timing buffer");
+          std::vector<unsigned long long> init = {~0ULL, 0ULL, 0ULL};
+          cuda_check(cudaMemcpyAsync(timing_buf + 3 * ui, init.data(), 24, cudaMemcpyHostToDevice, K), "timing");
+          cuda_check(cudaStreamSynchronize(K), "timing");
+          dd.timing = timing_buf + 3 * ui;
+          cuda_check(cudaEventCreate(&unit_ev[ui].first), "event");
+          cuda_check(cudaEventCreate(&unit_ev[ui].second), "event");
+          events.push_back(unit_ev[ui].first);
+          events.push_back(unit_ev[ui].second);
+          cuda_check(cudaEventRecord(unit_ev[ui].first, K), "event");
+        }
+        dual_launch(dd, flops_d, flops_f, K);
+        if (log_units) cuda_check(cudaEventRecord(unit_ev[ui].second, K), "event");
+        if (fc)
+          for (const std::vector<size_t>* lst : {&u.d, &u.f})
+            for (size_t i : *lst) fc->add(reference_flops(cs[i].plan));
+      }
+      k_done[ui] = ev();
+      cuda_check(cudaEventRecord(k_done[ui], K), "event");
+    }
+    // results back to the host (every host C, after the last launch), residents released
+    cuda_check(cudaStreamWaitEvent(S.out, k_done.empty() ? fork : k_done.back(), 0), "join");
+    for (auto& rs : residents) {
+      bool written = false;
+      for (const Call& c : cs)
+        if (c.host[2] && rs.first.contains(c.win[2])) written = true;
+      if (!written) continue;
+      cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(rs.first.lo), rs.second, rs.first.bytes(),
+                                 cudaMemcpyDeviceToHost, S.out),
+                 "D2H staging");
+      g_d2h_bytes.fetch_add(rs.first.bytes(), std::memory_order_relaxed);
+    }
+    for (auto& rs : residents) cuda_check(cudaFreeAsync(rs.second, S.out), "staging release");
+    residents.clear();
+    for (void*& a : arena)
+      if (a) {
+        cuda_check(cudaFreeAsync(a, S.out), "workspace release");
+        a = nullptr;
+      }
+    cudaEvent_t done = ev();
+    cuda_check(cudaEventRecord(done, S.out), "event");
+    cuda_check(cudaStreamWaitEvent(user, done, 0), "join");
+    if (sync) cuda_check(cudaStreamSynchronize(user), "gemm synchronisation");
+    if (log_units) {  // measured device time of every launch next to its estimate
+      cuda_check(cudaEventSynchronize(done), "event");
+      std::vector<unsigned long long> tm(units.size() * 3, 0);
+      if (timing_buf) {
+        cuda_check(cudaMemcpy(tm.data(), timing_buf, tm.size() * 8, cudaMemcpyDeviceToHost), "timing");
+        cudaFree(timing_buf);
+      }
+      if (FILE* f = std::fopen(log_path, "a")) {
+        for (size_t ui = 0; ui < units.size(); ++ui) {
+          if (!unit_ev[ui].first) continue;
+          float ms = 0;
+          cudaEventElapsedTime(&ms, unit_ev[ui].first, unit_ev[ui].second);
+          double td = 0, tf = 0, fd = 0, ff = 0;
+          for (size_t i : units[ui].d) {
+            td += est[i];
+            fd += 2.0 * cs[i].plan.m * cs[i].plan.n * cs[i].plan.k;
+          }
+          for (size_t i : units[ui].f) {
+            tf += est[i];
+            ff += 2.0 * cs[i].plan.m * cs[i].plan.n * cs[i].plan.k;
+          }
+          const double dend = tm[3 * ui + 1] > tm[3 * ui] ? (tm[3 * ui + 1] - tm[3 * ui]) * 1e-6 : 0.0;
+          const double fend = tm[3 * ui + 2] > tm[3 * ui] ? (tm[3 * ui + 2] - tm[3 * ui]) * 1e-6 : 0.0;
+          std::fprintf(f,
+                       "  launch %3zu: D %2zu est %7.3f end %7.3f | F %2zu est %7.3f end %7.3f | measured %7.3f ms | "
+                       "%.1f + %.1f TF/s\n",
+                       ui, units[ui].d.size(), td * 1e3, dend, units[ui].f.size(), tf * 1e3, fend, ms, fd / ms / 1e9,
+                       ff / ms / 1e9);
+        }
+        std::fclose(f);
+      }
+    }
+    failed = false;
+  } catch (...) {
+    cleanup(true);
+    throw;
+  }
+  cleanup(failed);
+  return true;
+}
+
 void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc) {
   // Every plan first: policy and shape errors surface before any device work.
   std::vector<Call> cs(calls.size());
@@ -193,6 +622,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     }
   }
   const Streams S = device_streams();
+  if (try_run_dual(cs, cfg, S, user, sync, fc)) return;
   static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..8 concurrent compute streams
     const char* f = std::getenv("MDGEMM_STREAMS");
     const int v = f ? std::atoi(f) : 4;  // default four concurrent streams

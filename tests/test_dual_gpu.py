@@ -1,0 +1,113 @@
+"""The dual-pipe kernel (gemm_dual.cu) behind gemm_batch: FP64 DMMA jobs and
+FP32 FFMA2 jobs of one batch share every SM.  Its results must be BITWISE the
+results of calling gemm() on each call in order (same k order, same DMMA /
+FFMA2 rounding, same accumulate_element combine), for every label, C layout,
+edge tile, dependency chain, host or device operands."""
+import numpy as np
+import pytest
+
+import paper_1901_06015_b200 as M
+from oracle import oracle as O
+from tests.helpers import HostMatrix, Problem, SCALARS, config
+
+pytestmark = pytest.mark.gpu
+
+LABELS = [l.str() for l in M.CaseLabel.all()]
+SHAPES = [(70, 65, 80), (129, 200, 33), (64, 128, 16), (5, 3, 1), (200, 129, 257), (1, 300, 7)]
+
+
+def _alpha(label):
+    cid = M.CaseLabel.parse(label).case_id()
+    return SCALARS["cfg2_alpha"] if cid in (0, 7) else SCALARS["p7"]
+
+
+def _batch_with_profile(calls, cfg):
+    M.profile_begin()
+    M.gemm_batch(calls, cfg)
+    return M.profile_end()
+
+
+@pytest.mark.parametrize("c_kind", ["col", "row"])
+def test_dual_all_labels_equal_single_calls(monkeypatch, c_kind):
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    probs = [Problem(l, *SHAPES[i % len(SHAPES)], c_kind=c_kind, seed=7 + i, trans_a=(i % 5 == 3))
+             for i, l in enumerate(LABELS)]
+    want = []
+    for p in probs:
+        c = p.C.clone()
+        va, vb, vc = p.views(C=c)
+        M.gemm(_alpha(p.label), va, vb, SCALARS["cfg2_beta"], vc, cfg)
+        want.append(c)
+    calls = []
+    for p in probs:
+        va, vb, vc = p.views()
+        calls.append((_alpha(p.label), va, vb, SCALARS["cfg2_beta"], vc))
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] > 0, ks
+    for p, w in zip(probs, want):
+        assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
+
+
+@pytest.mark.parametrize("beta", ["cfg2_beta", "one", "zero"])
+def test_dual_chains_equal_sequential_calls(monkeypatch, beta):
+    """Calls sharing one host C per C datatype (dependency chains that alternate
+    computation precisions): the list schedule must keep every chain's order."""
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    shared = {dt: HostMatrix(dt, 96, 140).fill(O.orc_rng_state(11, ["c", dt])) for dt in range(4)}
+    ref = {dt: h.clone() for dt, h in shared.items()}
+    probs = [Problem(l, 96, 140, 72, seed=i) for i, l in enumerate(LABELS)]
+    for p in probs:
+        va, vb, _ = p.views()
+        M.gemm(_alpha(p.label), va, vb, SCALARS[beta], ref[p.C.dtype].view(comp=p.comp), cfg)
+    calls = []
+    for p in probs:
+        va, vb, _ = p.views()
+        calls.append((_alpha(p.label), va, vb, SCALARS[beta], shared[p.C.dtype].view(comp=p.comp)))
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] > 0 and ks["dual_f"]["work"] > 0, ks
+    for dt in range(4):
+        assert shared[dt].buf.tobytes() == ref[dt].buf.tobytes(), dt
+
+
+def test_dual_device_operands_and_raw_chain(monkeypatch):
+    """Device operands, a later call reading an earlier call's C as its A
+    (the pack must wait for that launch), k = 0 and empty calls in between."""
+    import torch
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    n = 136
+    mats = {name: HostMatrix(M.DT_D if name < "N" else M.DT_S, n, n).fill(O.orc_rng_state(5, [name]))
+            for name in ["A", "B", "C", "D", "E", "P", "Q", "R", "S"]}
+    seq = [("A", "B", "C", 136), ("P", "Q", "R", 136), ("C", "B", "D", 136),  # D reads C (RAW through A)
+           ("R", "Q", "S", 136), ("A", "D", "E", 0), ("P", "S", "R", 136), ("E", "B", "C", 136)]
+    ref = {k: v.clone() for k, v in mats.items()}
+
+    def view(store, name, k, role):
+        h = store[name]
+        v = h.view()
+        if role == "a":
+            v = M.MatrixView.make(v.base, n, k, 1, n, v.dtype)
+        elif role == "b":
+            v = M.MatrixView.make(v.base, k, n, 1, max(k, 1), v.dtype)
+        return v
+    for a, b, c, k in seq:
+        M.gemm(SCALARS["p7"], view(ref, a, k, "a"), view(ref, b, k, "b"), SCALARS["m3"], ref[c].view(), cfg)
+    dev = {k: v.to_device() for k, v in mats.items()}
+    calls = [(SCALARS["p7"], view(dev, a, k, "a"), view(dev, b, k, "b"), SCALARS["m3"], dev[c].view())
+             for a, b, c, k in seq]
+    ks = _batch_with_profile(calls, cfg)
+    torch.cuda.synchronize()
+    assert ks["dual_d"]["launches"] > 0, ks
+    for k in mats:
+        assert dev[k].bytes().tobytes() == ref[k].buf.tobytes(), k
+
+
+def test_dual_off_and_exact_take_the_stream_scheduler(monkeypatch):
+    probs = [Problem(l, 40, 40, 40, seed=3) for l in ("dddd", "ssss", "zzzd", "cccs")]
+    for env, numerics in (("0", "fast"), ("1", "exact")):
+        monkeypatch.setenv("MDGEMM_DUAL", env)
+        calls = [(SCALARS["p7"], *p.views()[:2], SCALARS["one"], p.views()[2]) for p in probs]
+        ks = _batch_with_profile(calls, config({"gpu.numerics": numerics}))
+        assert ks["dual_d"]["launches"] == 0, (env, numerics)
