@@ -60,6 +60,9 @@ def parse_args():
     ap.add_argument("--numerics", choices=["fast", "exact"], default="fast")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-serial", action="store_true",
+                    help="skip the serialized per-call pass (per-case rates, classic-kernel rooflines); "
+                         "for ncu launch lists of the batched step alone")
     ap.add_argument("--cpu-size", type=int, default=512, help="sample size of the CPU baseline")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
@@ -259,19 +262,30 @@ def run_b200(args):
     clocks = sampler.stop()
     total_ms = sum(step_ms)
 
+    # Kernels of the timed step itself: one more step of the same batch with the
+    # library's per-launch CUDA events (each dual-pipe launch is bracketed on its
+    # own stream after its packs, so its span is its own duration).
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    M.profile_begin()
+    step()
+    torch.cuda.synchronize()
+    bstats = M.profile_end()
+
     # Per-kernel roofline: inside the timed steps independent calls overlap on
     # several streams, so a launch's event span is not its own duration; one
     # extra step runs the same calls serialized on the timed stream, each
     # kernel bracketed by CUDA events (mdg_profile_begin/end).
     # (an untimed serialized pass first: isolated calls may use kernel variants
     # the batched steps never launched, and CUDA loads modules lazily)
-    for al, va, vb, be, vc in calls:
+    serial_calls = [] if args.no_serial else calls
+    for al, va, vb, be, vc in serial_calls:
         M.gemm_async(al, va, vb, be, vc, cfg, stream)
     flush.fill_(1)
     torch.cuda.synchronize()
     M.profile_begin()
     call_events = []
-    for al, va, vb, be, vc in calls:
+    for al, va, vb, be, vc in serial_calls:
         ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         ev[0].record(stream)
         M.gemm_async(al, va, vb, be, vc, cfg, stream)
@@ -305,13 +319,33 @@ def run_b200(args):
                   for l, m, n, k, _, _ in items) * args.steps
     peak_fraction = ideal_s / (total_ms * 1e-3)
 
-    # roofline of the dominant kernel (rank 0's launches)
+    # roofline of the dominant kernel of the timed step (rank 0's launches)
+    traffic_map = json.load(open(TRAFFIC_FILE)) if os.path.exists(TRAFFIC_FILE) else {}
+    batch_kinds = {k: v for k, v in bstats.items() if v["ms"] > 0 and k != "dual_f"}
+    dual = bstats.get("dual_d", {"ms": 0.0})
     dom = max(("dmma", "ffma", "pack"), key=lambda k: kstats[k]["ms"])
     ks = kstats[dom]
-    traffic = None
-    if os.path.exists(TRAFFIC_FILE):
-        traffic = json.load(open(TRAFFIC_FILE)).get(dom)
-    if dom == "pack":
+    traffic = traffic_map.get(dom)
+    if batch_kinds and max(batch_kinds, key=lambda k: batch_kinds[k]["ms"]) == "dual_d":
+        # Both pipes at once: the roofline is the serialized pipe mix of the same flops
+        # (the time the DMMA flops take at the FP64 peak plus the FFMA flops at the FP32
+        # peak); frac > 1 means the kernel beats running the pipes one after the other.
+        fd, ff, ms = dual["work"], bstats["dual_f"]["work"], dual["ms"]
+        achieved = (fd + ff) / (ms * 1e-3) / 1e12
+        serial_peak = (fd + ff) / (fd / pk["dmma_tflops"] + ff / pk["ffma_tflops"]) if fd + ff else 0.0
+        roof = {"bound": "tensor", "achieved": achieved, "peak": serial_peak, "unit": "TFLOP/s",
+                "frac": achieved / serial_peak if serial_peak else 0.0, "traffic": traffic_map.get("dual"),
+                "kernel": "gemm_dual: FP64 DMMA.8x8x4 warps + FP32 FFMA2 warps on every SM at once",
+                "pipes": {"dmma": {"achieved": fd / (ms * 1e-3) / 1e12, "peak": pk["dmma_tflops"],
+                                   "frac": fd / (ms * 1e-3) / 1e12 / pk["dmma_tflops"]},
+                          "ffma": {"achieved": ff / (ms * 1e-3) / 1e12, "peak": pk["ffma_tflops"],
+                                   "frac": ff / (ms * 1e-3) / 1e12 / pk["ffma_tflops"]}},
+                "launches": dual["launches"], "kernel_ms_per_step": ms,
+                "peak_source": "serialized mix of the measured DMMA / FFMA peaks (profiles/peaks_r01.json) for "
+                               "this step's flops",
+                "algorithmic_work": "2*me*ne*ke real flops per job (= flops_of_case)",
+                "measured": "one extra step of the same batch, CUDA events around every launch"}
+    elif dom == "pack":
         achieved = ks["work"] / (ks["ms"] * 1e-3) / 1e9 if ks["ms"] else 0.0
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "pack",
@@ -324,7 +358,7 @@ def run_b200(args):
                 "kernel": "gemm_dmma (DMMA.8x8x4 fp64 tensor pipe)" if dom == "dmma" else "gemm_ffma (FFMA fp32)",
                 "peak_source": "measured: tools/peaks.cu on this pool's B200 (profiles/peaks_r01.json)",
                 "algorithmic_work": "2*me*ne*ke real flops per launch (= flops_of_case, the 1m reduction has no waste)"}
-    roof["measured"] = "one serialized step after the timed region, CUDA events around every launch"
+    roof.setdefault("measured", "one serialized step after the timed region, CUDA events around every launch")
     kernels = {}
     for kind, v in kstats.items():
         if not v["launches"] or not v["ms"]:
@@ -401,6 +435,8 @@ def run_b200(args):
         "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},
         "roofline": roof,
         "kernel_share": kernel_share,
+        "step_kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3)} for k, v in bstats.items()
+                         if v["launches"] or v["ms"]},
         "kernels": kernels,
         "per_case": per_case,
         "serialized_step_ms": serial_ms,

@@ -436,19 +436,36 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     cudaEvent_t fork = ev();
     cuda_check(cudaEventRecord(fork, user), "event");
     for (cudaStream_t st : {S.in, K, P, S.out}) cuda_check(cudaStreamWaitEvent(st, fork, 0), "fork");
-    // host operands: one resident copy per distinct window
-    for (const Window& w : all) {
+    // host operands: one resident copy per distinct window, copied in the
+    // order the schedule first needs them; every launch waits only for the
+    // copies of its own operands, and a host C goes back right after the last
+    // launch writing it
+    std::vector<long> first_use(all.size(), -1), last_write(all.size(), -1);
+    std::vector<std::vector<size_t>> call_res(n);
+    for (size_t i = 0; i < n; ++i)
+      for (int r = 0; r < 3; ++r) {
+        if (!cs[i].host[r]) continue;
+        for (size_t x = 0; x < all.size(); ++x)
+          if (all[x].contains(cs[i].win[r])) {
+            call_res[i].push_back(x);
+            const long u = unit_of[i];
+            if (first_use[x] < 0 || u < first_use[x]) first_use[x] = u;
+            if (r == 2) last_write[x] = std::max(last_write[x], u);
+          }
+      }
+    std::vector<size_t> order(all.size());
+    for (size_t x = 0; x < all.size(); ++x) order[x] = x;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return first_use[a] < first_use[b]; });
+    std::vector<cudaEvent_t> staged(all.size(), nullptr);
+    residents.resize(all.size());
+    for (size_t x : order) {
       void* d = nullptr;
-      cuda_check(cudaMallocAsync(&d, w.bytes(), S.in), "staging allocation");
-      residents.emplace_back(w, static_cast<std::byte*>(d));
-      cuda_check(cudaMemcpyAsync(d, w.lo, w.bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
-      g_h2d_bytes.fetch_add(w.bytes(), std::memory_order_relaxed);
-    }
-    if (!all.empty()) {
-      cudaEvent_t staged = ev();
-      cuda_check(cudaEventRecord(staged, S.in), "event");
-      cuda_check(cudaStreamWaitEvent(K, staged, 0), "dependency");
-      cuda_check(cudaStreamWaitEvent(P, staged, 0), "dependency");
+      cuda_check(cudaMallocAsync(&d, all[x].bytes(), S.in), "staging allocation");
+      residents[x] = {all[x], static_cast<std::byte*>(d)};
+      cuda_check(cudaMemcpyAsync(d, all[x].lo, all[x].bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
+      g_h2d_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
+      staged[x] = ev();
+      cuda_check(cudaEventRecord(staged[x], S.in), "event");
     }
     auto rebase = [&](size_t i) {
       Call& c = cs[i];
@@ -461,6 +478,17 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
         for (MatrixView* v : {&p.a, &p.b, &p.c})
           if (v->base >= c.win[r].lo && v->base < c.win[r].hi) v->base = base + (v->base - c.win[r].lo);
       }
+    };
+    // the streams wait for the copies a unit's calls read (once per resident and stream)
+    std::vector<char> waited_k(all.size(), 0), waited_p(all.size(), 0);
+    auto wait_inputs = [&](const std::vector<size_t>& members, bool on_p) {
+      for (size_t i : members)
+        for (size_t x : call_res[i]) {
+          std::vector<char>& w = on_p ? waited_p : waited_k;
+          if (w[x]) continue;
+          w[x] = 1;
+          cuda_check(cudaStreamWaitEvent(on_p ? P : K, staged[x], 0), "dependency");
+        }
     };
     for (size_t i = 0; i < n; ++i) rebase(i);
     if (arena_bytes > 0)
@@ -476,6 +504,11 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     }
     for (size_t ui = 0; ui < units.size(); ++ui) {
       const Unit& u = units[ui];
+      std::vector<size_t> members = u.d;
+      members.insert(members.end(), u.f.begin(), u.f.end());
+      if (u.classic >= 0) members.push_back(static_cast<size_t>(u.classic));
+      wait_inputs(members, false);
+      if (u.classic < 0) wait_inputs(members, true);
       if (u.classic >= 0) {
         Call& c = cs[static_cast<size_t>(u.classic)];
         execute_scheduled(c.plan, cfg.numerics, K, fc, true);
@@ -531,19 +564,20 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       }
       k_done[ui] = ev();
       cuda_check(cudaEventRecord(k_done[ui], K), "event");
+      // host results this launch wrote for the last time
+      bool any = false;
+      for (size_t x = 0; x < all.size(); ++x)
+        if (last_write[x] == static_cast<long>(ui)) {
+          if (!any) cuda_check(cudaStreamWaitEvent(S.out, k_done[ui], 0), "dependency");
+          any = true;
+          cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(all[x].lo), residents[x].second, all[x].bytes(),
+                                     cudaMemcpyDeviceToHost, S.out),
+                     "D2H staging");
+          g_d2h_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
+        }
     }
     // results back to the host (every host C, after the last launch), residents released
     cuda_check(cudaStreamWaitEvent(S.out, k_done.empty() ? fork : k_done.back(), 0), "join");
-    for (auto& rs : residents) {
-      bool written = false;
-      for (const Call& c : cs)
-        if (c.host[2] && rs.first.contains(c.win[2])) written = true;
-      if (!written) continue;
-      cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(rs.first.lo), rs.second, rs.first.bytes(),
-                                 cudaMemcpyDeviceToHost, S.out),
-                 "D2H staging");
-      g_d2h_bytes.fetch_add(rs.first.bytes(), std::memory_order_relaxed);
-    }
     for (auto& rs : residents) cuda_check(cudaFreeAsync(rs.second, S.out), "staging release");
     residents.clear();
     for (void*& a : arena)
