@@ -111,3 +111,53 @@ def test_dual_off_and_exact_take_the_stream_scheduler(monkeypatch):
         calls = [(SCALARS["p7"], *p.views()[:2], SCALARS["one"], p.views()[2]) for p in probs]
         ks = _batch_with_profile(calls, config({"gpu.numerics": numerics}))
         assert ks["dual_d"]["launches"] == 0, (env, numerics)
+
+
+@pytest.mark.parametrize("variant", ["gen_c", "conj", "trans_b", "k_ragged"])
+def test_dual_variants_equal_single_calls(monkeypatch, variant):
+    """General-stride C (gaps between elements), conjugated operands, transposed B and inner
+    dimensions that are not multiples of the 16-deep k-block, every label."""
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    kw = {"gen_c": dict(c_kind="gen"), "conj": dict(conj_a=True, conj_b=True), "trans_b": dict(trans_b=True),
+          "k_ragged": {}}[variant]
+    shape = (37, 41, 23) if variant == "k_ragged" else (72, 136, 48)
+    probs = [Problem(l, *shape, seed=100 + i, **kw) for i, l in enumerate(LABELS)]
+    want = []
+    for p in probs:
+        c = p.C.clone()
+        va, vb, vc = p.views(C=c)
+        M.gemm(_alpha(p.label), va, vb, SCALARS["m3"], vc, cfg)
+        want.append(c)
+    calls = [(_alpha(p.label), *p.views()[:2], SCALARS["m3"], p.views()[2]) for p in probs]
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] > 0, ks
+    for p, w in zip(probs, want):
+        assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
+
+
+def test_dual_within_fast_tolerance_of_oracle(monkeypatch):
+    """Independent of the classic kernels: dual results against the CPU oracle (the reference's
+    per-element criterion and the north-star relative Frobenius bound, as in test_gemm_fast_gpu)."""
+    from tests.test_gemm_fast_gpu import frob_bound
+    from tests.helpers import rel_frobenius
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    probs = [Problem(l, 33, 70, 129, seed=300 + i) for i, l in enumerate(LABELS[::3])]
+    orig = [p.C.clone() for p in probs]
+    want = []
+    for p in probs:
+        c = p.C.clone()
+        va, vb, vc = p.views(C=c)
+        O.orc_gemm(_alpha(p.label), va, vb, SCALARS["cfg2_beta"], vc, config({}))
+        want.append(c)
+    calls = [(_alpha(p.label), *p.views()[:2], SCALARS["cfg2_beta"], p.views()[2]) for p in probs]
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] > 0, ks
+    for p, w, o in zip(probs, want, orig):
+        va, vb, _ = p.views()
+        viol = O.orc_violation(_alpha(p.label), va, vb, SCALARS["cfg2_beta"], o.view(comp=p.comp),
+                               p.C.view(comp=p.comp), p.comp)
+        assert viol <= 1.0, (p.label, viol)
+        err = rel_frobenius(p.C.values(), w.values())
+        assert err <= frob_bound(p.label, p.k), (p.label, err)
