@@ -123,7 +123,7 @@ constexpr int TRACE_WORDS = 6;
 // One job of the dual-pipe kernel (gemm_dual.cu): a FAST gemm whose operands
 // are already packed with the group's tile as panel dimension (D group:
 // 128-row A panels, 128-column B panels, doubles; F group: 64 / 128, floats)
-// and panel length lpad (a multiple of 16).
+// and panel length lpad (a multiple of the group's k-block: 16 / 32).
 struct DualJob {
   const void* a;
   const void* b;
@@ -145,7 +145,7 @@ struct DualDesc {
   DualJob d[DUAL_MAX_JOBS];
   DualJob f[DUAL_MAX_JOBS];
 };
-constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128, DUAL_BK = 16;
+constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128, DUAL_BK = 16, DUAL_F_BK = 32;
 
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);

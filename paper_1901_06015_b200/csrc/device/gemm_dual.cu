@@ -11,7 +11,9 @@
 //               FFMA kernels' mainloop); setmaxnreg 144;
 //   warp 12     D producer lane: TMA bulk copies of 16-deep slabs into the
 //               D ring (3 x 32 KB);
-//   warp 13     F producer lane: the same into the F ring (6 x 12 KB);
+//   warp 13     F producer lane: 32-deep slabs into the F ring (4 x 24 KB;
+//               32-deep halves the per-stage barrier / proxy-fence cost
+//               that a single FFMA2 warp per sub-partition cannot hide);
 //   warps 14-15 idle (the producer warpgroup gives its registers away:
 //               setmaxnreg 32; 256 x 168 + 128 x 144 + 128 x 32 = 64 K).
 //
@@ -38,11 +40,12 @@
 namespace mdg {
 namespace {
 
-constexpr int DU_BK = 16;
+constexpr int DU_BK = DUAL_BK;      // D group k-block
+constexpr int DF_BK = DUAL_F_BK;    // F group k-block
 constexpr int DD_BM = 128, DD_BN = 128;  // D tile; 8 warps (2 x 4) of 64x32
 constexpr int DF_BM = 64, DF_BN = 128;   // F tile; 128 threads (8 x 16) of 8x8
 constexpr int DD_SA = DU_BK * DD_BM, DD_SB = DU_BK * DD_BN;  // doubles per stage
-constexpr int DF_SA = DU_BK * DF_BM, DF_SB = DU_BK * DF_BN;  // floats per stage
+constexpr int DF_SA = DF_BK * DF_BM, DF_SB = DF_BK * DF_BN;  // floats per stage
 template <int DD_STAGES, int DF_STAGES>
 struct DuRings {
   static constexpr size_t DD_RING = size_t(DD_STAGES) * (DD_SA + DD_SB) * sizeof(double);
@@ -247,8 +250,10 @@ __device__ __forceinline__ void prefetch_c(const DualJob& jb, int tm, int tn, in
   }
 }
 
-template <int DD_STAGES, int DF_STAGES>
-__global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_constant__ DualDesc d) {
+// Register split per warp group (setmaxnreg): RP producers, RD DMMA warps,
+// RF FFMA2 warps; RP*128 + RD*256 + RF*128 = the CTA's launch allocation.
+template <int DD_STAGES, int DF_STAGES, int RP, int RD, int RF>
+__device__ __forceinline__ void dual_body(const DualDesc& d) {
   constexpr size_t DD_RING = DuRings<DD_STAGES, DF_STAGES>::DD_RING;
   constexpr size_t DF_RING = DuRings<DD_STAGES, DF_STAGES>::DF_RING;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -277,7 +282,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
   __syncthreads();
 
   if (warp >= DD_PROD_WARP) {  // ------------------------------------------ producers
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RP));
     if (lane != 0) return;
     if (warp == DD_PROD_WARP) {
       int it = 0;
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
         if (d.prefetch_c) prefetch_c(jb, tm, tn, DF_BM, DF_BN);
         const float* Ag = static_cast<const float*>(jb.a) + static_cast<int64_t>(tm) * DF_BM * jb.lpad;
         const float* Bg = static_cast<const float*>(jb.b) + static_cast<int64_t>(tn) * DF_BN * jb.lpad;
-        const int nk = static_cast<int>(jb.lpad / DU_BK);
+        const int nk = static_cast<int>(jb.lpad / DF_BK);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % DF_STAGES;
           if (it >= DF_STAGES) mbar_wait(&fempty[s], ((it / DF_STAGES) - 1) & 1);
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
   }
 
   if (warp < DD_WARPS) {  // ----------------------------------------------- D group
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RD));
     const int wm = warp % 2, wn = warp / 2;
     const int g = lane >> 2, tig = lane & 3;
     const double* a_base = dA + wm * 64 + g + tig * DD_BM;
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
   }
 
   // ------------------------------------------------------------------- F group
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 144;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RF));
   const int ft = threadIdx.x - DD_WARPS * 32;
   const int tx = ft % 16, ty = ft / 16;
   const float* a_base = fA + ty * 4;
@@ -385,7 +390,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
       const DualJob& jb = d.f[jx];
       tile_coords(v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
     }
-    const int nk = static_cast<int>(d.f[jx].lpad / DU_BK);
+    const int nk = static_cast<int>(d.f[jx].lpad / DF_BK);
     uint64_t acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -397,7 +402,7 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
       const float* a = a_base + s * DF_SA;
       const float* b = b_base + s * DF_SB;
 #pragma unroll
-      for (int kk = 0; kk < DU_BK; ++kk) {
+      for (int kk = 0; kk < DF_BK; ++kk) {
         const float4 a0 = *reinterpret_cast<const float4*>(a + kk * DF_BM);
         const float4 a1 = *reinterpret_cast<const float4*>(a + kk * DF_BM + DF_BM / 2);
         const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(b + kk * DF_BN);
@@ -423,29 +428,36 @@ __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_c
   if (d.timing && lane == 0) atomicMax(&d.timing[2], globaltimer());
 }
 
+// The whole register file (128 per thread at launch: 256 x 168 + 128 x 144 +
+// 128 x 32 = 64 K).
+template <int DD_STAGES, int DF_STAGES>
+__global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_constant__ DualDesc d) {
+  dual_body<DD_STAGES, DF_STAGES, 32, 168, 144>(d);
+}
+
 template <int DS, int FS>
 cudaError_t launch_stages(const DualDesc& d, int grid, cudaStream_t s) {
   constexpr size_t smem = DuRings<DS, FS>::SMEM;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(gemm_dual_kernel<DS, FS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  auto kern = gemm_dual_kernel<DS, FS>;
+  cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
-  gemm_dual_kernel<DS, FS><<<static_cast<unsigned>(grid), DU_THREADS, smem, s>>>(d);
+  kern<<<static_cast<unsigned>(grid), DU_THREADS, smem, s>>>(d);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t dual_smem() { return DuRings<3, 6>::SMEM; }
+size_t dual_smem() { return DuRings<3, 4>::SMEM; }
 
 cudaError_t launch_gemm_dual(const DualDesc& d, int grid, cudaStream_t s) {
   if (grid <= 0 || (d.tiles_d == 0 && d.tiles_f == 0)) return cudaSuccess;
-  static const int variant = [] {  // tuning: MDGEMM_DUAL_STAGES = 0 (3 D / 6 F), 1 (3 / 10), 2 (4 / 8)
+  static const int variant = [] {  // tuning: MDGEMM_DUAL_STAGES = 0 (3 D / 4 F), 1 (3 / 5), 2 (4 / 4)
     const char* f = std::getenv("MDGEMM_DUAL_STAGES");
     return f ? std::atoi(f) : 0;
   }();
-  if (variant == 1) return launch_stages<3, 10>(d, grid, s);
-  if (variant == 2) return launch_stages<4, 8>(d, grid, s);
-  return launch_stages<3, 6>(d, grid, s);
+  if (variant == 1) return launch_stages<3, 5>(d, grid, s);
+  if (variant == 2) return launch_stages<4, 4>(d, grid, s);
+  return launch_stages<3, 4>(d, grid, s);
 }
 
 }  // namespace mdg

@@ -559,7 +559,8 @@ DualPrep dual_prepare(const ExecutionPlan& p) {
   d.single = p.comp_prec == Precision::Single;
   const int64_t bm = d.single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
   const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
-  d.lpad = (p.k + mdg::DUAL_BK - 1) / mdg::DUAL_BK * mdg::DUAL_BK;
+  const int64_t bk = d.single ? mdg::DUAL_F_BK : mdg::DUAL_BK;
+  d.lpad = (p.k + bk - 1) / bk * bk;
   const Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, bm, d.lpad);
   const Packed pb = prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, bn, d.lpad);
   d.pa = pa.desc;

@@ -184,9 +184,9 @@ size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
 namespace {
 
 // device rates of the two groups while both run, measured per launch on the
-// cfg2 sweep (MDGEMM_DUAL_LOG: group end times): 27.3 + 29.6 TFLOP/s
+// cfg2 sweep (MDGEMM_DUAL_LOG: group end times): 27.3 + 30.7 TFLOP/s
 // (tools/dual_probe's register-light loops: 28.7 + 34.9)
-constexpr double kDualRateD = 27.3e12, kDualRateF = 29.6e12;
+constexpr double kDualRateD = 27.3e12, kDualRateF = 30.7e12;
 
 struct Unit {
   std::vector<size_t> d, f;  // dual jobs (call indices)
@@ -305,13 +305,21 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   }
 
   // ---- list schedule
+  double rate_d = kDualRateD, rate_f = kDualRateF;
+  if (const char* f = std::getenv("MDGEMM_DUAL_RATES")) {  // tuning: "D,F" in TFLOP/s
+    double a = 0, b = 0;
+    if (std::sscanf(f, "%lf,%lf", &a, &b) == 2 && a > 0 && b > 0) {
+      rate_d = a * 1e12;
+      rate_f = b * 1e12;
+    }
+  }
   std::vector<DualPrep> prep(n);
   std::vector<double> est(n, 0.0);
   size_t max_call_bytes = 0;
   for (size_t i = 0; i < n; ++i)
     if (kind[i]) {
       prep[i] = dual_prepare(cs[i].plan);
-      est[i] = prep[i].tile_flops / (kind[i] == 1 ? kDualRateD : kDualRateF);
+      est[i] = prep[i].tile_flops / (kind[i] == 1 ? rate_d : rate_f);
       max_call_bytes = std::max(max_call_bytes, prep[i].bytes);
     }
   const size_t unit_cap = std::max(max_call_bytes, size_t{6} << 30);  // packed bytes per launch
