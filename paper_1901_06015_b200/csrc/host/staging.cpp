@@ -417,7 +417,10 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   }
 
   // ---- emission
+  // K: the dual launches (and classic units) in order; P: packs, fanned out to
+  // PX so the many small pack kernels of a launch overlap each other
   cudaStream_t K = S.compute[0], P = S.compute[1];
+  const cudaStream_t PX[2] = {S.compute[2], S.compute[3]};
   std::vector<cudaEvent_t> events;
   auto ev = [&]() {
     events.push_back(new_event());
@@ -431,6 +434,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       cudaStreamSynchronize(S.in);
       cudaStreamSynchronize(K);
       cudaStreamSynchronize(P);
+      for (cudaStream_t q : PX) cudaStreamSynchronize(q);
       cudaStreamSynchronize(S.out);
       for (auto& r : residents) cudaFree(r.second);
       for (void* a : arena)
@@ -443,7 +447,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   try {
     cudaEvent_t fork = ev();
     cuda_check(cudaEventRecord(fork, user), "event");
-    for (cudaStream_t st : {S.in, K, P, S.out}) cuda_check(cudaStreamWaitEvent(st, fork, 0), "fork");
+    for (cudaStream_t st : {S.in, K, P, PX[0], PX[1], S.out}) cuda_check(cudaStreamWaitEvent(st, fork, 0), "fork");
     // host operands: one resident copy per distinct window, copied in the
     // order the schedule first needs them; every launch waits only for the
     // copies of its own operands, and a host C goes back right after the last
@@ -529,6 +533,11 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
             if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
         if (abw >= 0 && k_done[static_cast<size_t>(abw)])
           cuda_check(cudaStreamWaitEvent(P, k_done[static_cast<size_t>(abw)], 0), "dependency");
+        // fan out: PX inherit P's dependencies, P joins them after the packs
+        cudaEvent_t pgo = ev();
+        cuda_check(cudaEventRecord(pgo, P), "event");
+        for (cudaStream_t q : PX) cuda_check(cudaStreamWaitEvent(q, pgo, 0), "fork");
+        int npk = 0;
         mdg::DualDesc dd{};
         double flops_d = 0, flops_f = 0;
         char* w = static_cast<char*>(arena[ui % 2]);
@@ -539,7 +548,8 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
           int32_t tiles = 0;
           for (size_t x = 0; x < lst.size(); ++x) {
             const size_t i = lst[x];
-            dual_pack(cs[i].plan, w + off, P, &jobs[x]);
+            dual_pack(cs[i].plan, w + off, npk == 0 ? P : PX[npk - 1], &jobs[x]);
+            npk = (npk + 1) % 3;
             off += prep[i].bytes;
             jobs[x].tile0 = tiles;
             tiles += jobs[x].tiles_m * jobs[x].tiles_n;
@@ -548,6 +558,11 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
           }
           (grp == 0 ? dd.nd : dd.nf) = static_cast<int32_t>(lst.size());
           (grp == 0 ? dd.tiles_d : dd.tiles_f) = tiles;
+        }
+        for (cudaStream_t q : PX) {
+          cudaEvent_t j = ev();
+          cuda_check(cudaEventRecord(j, q), "event");
+          cuda_check(cudaStreamWaitEvent(P, j, 0), "join");
         }
         cudaEvent_t packed = ev();
         cuda_check(cudaEventRecord(packed, P), "event");
