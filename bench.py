@@ -321,12 +321,13 @@ def run_b200(args):
 
     # roofline of the dominant kernel of the timed step (rank 0's launches)
     traffic_map = json.load(open(TRAFFIC_FILE)) if os.path.exists(TRAFFIC_FILE) else {}
-    batch_kinds = {k: v for k, v in bstats.items() if v["ms"] > 0 and k != "dual_f"}
     dual = bstats.get("dual_d", {"ms": 0.0})
     dom = max(("dmma", "ffma", "pack"), key=lambda k: kstats[k]["ms"])
     ks = kstats[dom]
     traffic = traffic_map.get(dom)
-    if batch_kinds and max(batch_kinds, key=lambda k: batch_kinds[k]["ms"]) == "dual_d":
+    # (pack spans on their side streams include waiting for SMs the dual launches hold, so the
+    # dual kernel is the step's compute kernel whenever it ran)
+    if dual.get("launches", 0) > 0:
         # Both pipes at once: the roofline is the serialized pipe mix of the same flops
         # (the time the DMMA flops take at the FP64 peak plus the FFMA flops at the FP32
         # peak); frac > 1 means the kernel beats running the pipes one after the other.
