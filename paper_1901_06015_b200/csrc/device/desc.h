@@ -133,7 +133,9 @@ struct DualJob {
   DBeta beta;
   int32_t pair;
   int32_t tiles_m, tiles_n;
-  int32_t tile0;  // first virtual tile of the job in its group's list
+  int32_t tile0;       // first virtual tile of the job in its group's list
+  int32_t tile_begin;  // the job's first tile (raster order) in this launch
+  int32_t pad0;
 };
 constexpr int DUAL_MAX_JOBS = 80;  // per group and launch (kernel parameter space)
 struct DualDesc {

@@ -26,7 +26,8 @@
 // share an SM that way: two DMMA CTAs already fill its register file.
 //
 // Each group walks its jobs' tiles as one virtual index space (jobs sorted by
-// k on the host, longest first), CTA b taking tiles b, b + G, b + 2G, ...;
+// k on the host, longest first), CTA b taking one tile per round of G in
+// boustrophedon order (b, 2G-1-b, 2G+b, ...);
 // the two groups never synchronise with each other.  The epilogue combines
 // the accumulators straight into C through its strides (accumulate_element
 // via combine_typed, the classic kernels' arithmetic), so results are bitwise
@@ -60,6 +61,13 @@ __device__ __forceinline__ void dmma884_du(double& c0, double& c1, double a, dou
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// Virtual tile of CTA blockIdx.x in round r: boustrophedon order, so with the
+// tiles sorted longest-k first every CTA gets a similar total (round-robin
+// would hand the longest tile of every round to the same low CTA numbers).
+__device__ __forceinline__ int snake_tile(int r, int G) {
+  return r * G + ((r & 1) ? G - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x));
 }
 
 // Job of virtual tile v in a group's list (jobs' tile ranges are contiguous).
@@ -286,10 +294,12 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     if (lane != 0) return;
     if (warp == DD_PROD_WARP) {
       int it = 0;
-      for (int v = blockIdx.x; v < d.tiles_d; v += G) {
+      for (int r = 0; r * G < d.tiles_d; ++r) {
+        const int v = snake_tile(r, G);
+        if (v >= d.tiles_d) continue;
         const DualJob& jb = d.d[job_of(d.d, d.nd, v)];
         int tm, tn;
-        tile_coords(v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+        tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
         if (d.prefetch_c) prefetch_c(jb, tm, tn, DD_BM, DD_BN);
         const double* Ag = static_cast<const double*>(jb.a) + static_cast<int64_t>(tm) * DD_BM * jb.lpad;
         const double* Bg = static_cast<const double*>(jb.b) + static_cast<int64_t>(tn) * DD_BN * jb.lpad;
@@ -304,10 +314,12 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       }
     } else if (warp == DF_PROD_WARP) {
       int it = 0;
-      for (int v = blockIdx.x; v < d.tiles_f; v += G) {
+      for (int r = 0; r * G < d.tiles_f; ++r) {
+        const int v = snake_tile(r, G);
+        if (v >= d.tiles_f) continue;
         const DualJob& jb = d.f[job_of(d.f, d.nf, v)];
         int tm, tn;
-        tile_coords(v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+        tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
         if (d.prefetch_c) prefetch_c(jb, tm, tn, DF_BM, DF_BN);
         const float* Ag = static_cast<const float*>(jb.a) + static_cast<int64_t>(tm) * DF_BM * jb.lpad;
         const float* Bg = static_cast<const float*>(jb.b) + static_cast<int64_t>(tn) * DF_BN * jb.lpad;
@@ -332,12 +344,14 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     const double* b_base = dB + wn * 32 + g + tig * DD_BN;
     const uint32_t full_u = smem_u32(dfull), empty_u = smem_u32(dempty);
     int it = 0;
-    for (int v = blockIdx.x; v < d.tiles_d; v += G) {
+    for (int r = 0; r * G < d.tiles_d; ++r) {
+        const int v = snake_tile(r, G);
+        if (v >= d.tiles_d) continue;
       const int jx = job_of(d.d, d.nd, v);
       int tm, tn;
       {
         const DualJob& jb = d.d[jx];
-        tile_coords(v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+        tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
       }
       const int nk = static_cast<int>(d.d[jx].lpad / DU_BK);
       double acc[8][4][2];
@@ -383,12 +397,14 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   const float* b_base = fB + tx * 4;
   const uint32_t full_u = smem_u32(ffull), empty_u = smem_u32(fempty);
   int it = 0;
-  for (int v = blockIdx.x; v < d.tiles_f; v += G) {
+  for (int r = 0; r * G < d.tiles_f; ++r) {
+        const int v = snake_tile(r, G);
+        if (v >= d.tiles_f) continue;
     const int jx = job_of(d.f, d.nf, v);
     int tm, tn;
     {
       const DualJob& jb = d.f[jx];
-      tile_coords(v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+      tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
     }
     const int nk = static_cast<int>(d.f[jx].lpad / DF_BK);
     uint64_t acc[8][4];

@@ -571,6 +571,7 @@ DualPrep dual_prepare(const ExecutionPlan& p) {
   d.bytes = d.off_b + (pb.bytes + 255) / 256 * 256;
   d.tile_flops = 2.0 * static_cast<double>((p.m + bm - 1) / bm * bm) * static_cast<double>((p.n + bn - 1) / bn * bn) *
                  static_cast<double>(d.lpad);
+  d.tiles = static_cast<int32_t>(((p.m + bm - 1) / bm) * ((p.n + bn - 1) / bn));
   return d;
 }
 

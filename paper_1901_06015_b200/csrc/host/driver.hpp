@@ -63,6 +63,7 @@ struct DualPrep {
   int64_t lpad = 0;
   bool single = false;
   double tile_flops = 0.0;  // flops of the padded tile grid (2 tiles*BM*BN*lpad)
+  int32_t tiles = 0;        // tiles of the group's tile shape
 };
 DualPrep dual_prepare(const ExecutionPlan& p);
 // Launch the two pack kernels into ws (stream-ordered) and describe the job

@@ -188,10 +188,17 @@ namespace {
 // (tools/dual_probe's register-light loops: 28.7 + 34.9)
 constexpr double kDualRateD = 27.3e12, kDualRateF = 30.7e12;
 
+// A call's tile range [t0, t1) inside one launch: a long call may be split
+// over consecutive launches (its tiles are independent; each launch packs its
+// operands again) so that every launch pairs equal FP64 and FP32 work.
+struct Piece {
+  size_t call;
+  int32_t t0, t1;
+};
 struct Unit {
-  std::vector<size_t> d, f;  // dual jobs (call indices)
-  long classic = -1;         // or one call through execute()
-  size_t bytes = 0;          // packed operand bytes of the dual jobs
+  std::vector<Piece> d, f;  // dual jobs
+  long classic = -1;        // or one call through execute()
+  size_t bytes = 0;         // packed operand bytes of the dual jobs
 };
 
 int dual_mode() {
@@ -333,7 +340,12 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   }
   auto by_priority = [&](size_t x, size_t y) { return tail[x] != tail[y] ? tail[x] > tail[y] : x < y; };
   std::vector<Unit> units;
-  std::vector<long> unit_of(n, -1);
+  std::vector<long> unit_of(n, -1);     // last launch holding a piece of the call
+  std::vector<long> first_unit(n, -1);  // first one
+  std::vector<int32_t> next_tile(n, 0);
+  auto rem_est = [&](size_t i) {
+    return est[i] * static_cast<double>(prep[i].tiles - next_tile[i]) / static_cast<double>(prep[i].tiles);
+  };
   std::vector<size_t> ready;
   for (size_t i = 0; i < n; ++i)
     if (npred[i] == 0) ready.push_back(i);
@@ -346,51 +358,70 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       u.classic = static_cast<long>(*it);
     } else {
       double td = 0, tf = 0;
-      for (size_t i : ready) (kind[i] == 1 ? td : tf) += est[i];
+      for (size_t i : ready) (kind[i] == 1 ? td : tf) += rem_est(i);
       const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? td / 2 : td);
       const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? tf / 2 : tf);
-      // in priority order, jobs that keep each side within 5 % of its target;
-      // then, if a side fell short, its best remaining job (one overshoot)
+      // in priority order, whole remaining ranges that keep each side within
+      // 5 % of its target; then a side that fell short takes part of its next
+      // call's tiles
       double ad = 0, af = 0;
-      auto fits = [&](size_t i, bool loose) {
-        const bool isd = kind[i] == 1;
-        const std::vector<size_t>& lst = isd ? u.d : u.f;
-        const double acc = isd ? ad : af, target = isd ? target_d : target_f;
+      auto room = [&](size_t i) {
+        const std::vector<Piece>& lst = kind[i] == 1 ? u.d : u.f;
         if (lst.size() >= static_cast<size_t>(mdg::DUAL_MAX_JOBS)) return false;
-        if (!(u.d.empty() && u.f.empty()) && u.bytes + prep[i].bytes > unit_cap) return false;
-        if (lst.empty()) return true;
-        return loose ? acc < target * 0.95 : acc + est[i] <= target * 1.05;
+        return (u.d.empty() && u.f.empty()) || u.bytes + prep[i].bytes <= unit_cap;
       };
-      auto take = [&](size_t i) {
-        (kind[i] == 1 ? u.d : u.f).push_back(i);
-        (kind[i] == 1 ? ad : af) += est[i];
+      auto take = [&](size_t i, int32_t nt) {
+        const bool isd = kind[i] == 1;
+        (isd ? u.d : u.f).push_back(Piece{i, next_tile[i], next_tile[i] + nt});
+        (isd ? ad : af) += est[i] * nt / prep[i].tiles;
         u.bytes += prep[i].bytes;
       };
       std::vector<char> used(ready.size(), 0);
-      for (int pass = 0; pass < 2; ++pass)
-        for (size_t x = 0; x < ready.size(); ++x)
-          if (!used[x] && fits(ready[x], pass == 1)) {
-            take(ready[x]);
-            used[x] = 1;
-          }
+      for (size_t x = 0; x < ready.size(); ++x) {
+        const size_t i = ready[x];
+        const bool isd = kind[i] == 1;
+        const double acc = isd ? ad : af, target = isd ? target_d : target_f;
+        if (room(i) && acc + rem_est(i) <= target * 1.05) {
+          take(i, prep[i].tiles - next_tile[i]);
+          used[x] = 1;
+        }
+      }
+      for (size_t x = 0; x < ready.size(); ++x) {
+        const size_t i = ready[x];
+        const bool isd = kind[i] == 1;
+        const double acc = isd ? ad : af, target = isd ? target_d : target_f;
+        if (used[x] || !room(i) || (acc >= target * 0.95 && !(isd ? u.d : u.f).empty())) continue;
+        const int32_t left = prep[i].tiles - next_tile[i];
+        const double per_tile = est[i] / prep[i].tiles;
+        const int32_t want = static_cast<int32_t>(std::ceil((target - acc) / per_tile));
+        take(i, std::max<int32_t>(1, std::min(left, want)));
+        used[x] = 1;
+      }
     }
     const long uid = static_cast<long>(units.size());
-    std::vector<size_t> members = u.d;
-    members.insert(members.end(), u.f.begin(), u.f.end());
-    if (u.classic >= 0) members.push_back(static_cast<size_t>(u.classic));
-    for (size_t i : members) {
-      unit_of[i] = uid;
-      ready.erase(std::find(ready.begin(), ready.end(), i));
+    std::vector<size_t> finished;
+    for (std::vector<Piece>* lst : {&u.d, &u.f})
+      for (const Piece& pc : *lst) {
+        if (first_unit[pc.call] < 0) first_unit[pc.call] = uid;
+        unit_of[pc.call] = uid;
+        next_tile[pc.call] = pc.t1;
+        if (pc.t1 == prep[pc.call].tiles) finished.push_back(pc.call);
+      }
+    if (u.classic >= 0) {
+      unit_of[static_cast<size_t>(u.classic)] = uid;
+      first_unit[static_cast<size_t>(u.classic)] = uid;
+      finished.push_back(static_cast<size_t>(u.classic));
     }
-    done += members.size();
+    for (size_t i : finished) ready.erase(std::find(ready.begin(), ready.end(), i));
+    done += finished.size();
     std::vector<size_t> newly;
-    for (size_t i : members)
+    for (size_t i : finished)
       for (long s : succ[i])
         if (--npred[static_cast<size_t>(s)] == 0) newly.push_back(static_cast<size_t>(s));
     ready.insert(ready.end(), newly.begin(), newly.end());
     std::sort(ready.begin(), ready.end(), by_priority);
     // longest k first: the virtual tile order front-loads the longest tiles
-    auto by_k = [&](size_t x, size_t y) { return prep[x].lpad > prep[y].lpad; };
+    auto by_k = [&](const Piece& x, const Piece& y) { return prep[x.call].lpad > prep[y.call].lpad; };
     std::stable_sort(u.d.begin(), u.d.end(), by_k);
     std::stable_sort(u.f.begin(), u.f.end(), by_k);
     units.push_back(std::move(u));
@@ -402,8 +433,8 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       std::fprintf(f, "batch %zu calls -> %zu launches\n", n, units.size());
       for (const Unit& u : units) {
         double td = 0, tf = 0;
-        for (size_t i : u.d) td += est[i];
-        for (size_t i : u.f) tf += est[i];
+        for (const Piece& pc : u.d) td += est[pc.call] * (pc.t1 - pc.t0) / prep[pc.call].tiles;
+        for (const Piece& pc : u.f) tf += est[pc.call] * (pc.t1 - pc.t0) / prep[pc.call].tiles;
         std::fprintf(f, "  D %2zu jobs %8.3f ms | F %2zu jobs %8.3f ms | classic %ld | %.2f GB\n", u.d.size(), td * 1e3,
                      u.f.size(), tf * 1e3, u.classic, u.bytes / 1e9);
       }
@@ -461,7 +492,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
           if (all[x].contains(cs[i].win[r])) {
             call_res[i].push_back(x);
             const long u = unit_of[i];
-            if (first_use[x] < 0 || u < first_use[x]) first_use[x] = u;
+            if (first_use[x] < 0 || first_unit[i] < first_use[x]) first_use[x] = first_unit[i];
             if (r == 2) last_write[x] = std::max(last_write[x], u);
           }
       }
@@ -516,8 +547,9 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     }
     for (size_t ui = 0; ui < units.size(); ++ui) {
       const Unit& u = units[ui];
-      std::vector<size_t> members = u.d;
-      members.insert(members.end(), u.f.begin(), u.f.end());
+      std::vector<size_t> members;
+      for (const std::vector<Piece>* lst : {&u.d, &u.f})
+        for (const Piece& pc : *lst) members.push_back(pc.call);
       if (u.classic >= 0) members.push_back(static_cast<size_t>(u.classic));
       wait_inputs(members, false);
       if (u.classic < 0) wait_inputs(members, true);
@@ -528,9 +560,8 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
         // packs: after the kernel that last used this arena and after writers of the A/B read
         if (ui >= 2 && k_done[ui - 2]) cuda_check(cudaStreamWaitEvent(P, k_done[ui - 2], 0), "arena reuse");
         long abw = -1;
-        for (const std::vector<size_t>* lst : {&u.d, &u.f})
-          for (size_t i : *lst)
-            if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
+        for (size_t i : members)
+          if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
         if (abw >= 0 && k_done[static_cast<size_t>(abw)])
           cuda_check(cudaStreamWaitEvent(P, k_done[static_cast<size_t>(abw)], 0), "dependency");
         // fan out: PX inherit P's dependencies, P joins them after the packs
@@ -543,18 +574,19 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
         char* w = static_cast<char*>(arena[ui % 2]);
         size_t off = 0;
         for (int grp = 0; grp < 2; ++grp) {
-          const std::vector<size_t>& lst = grp == 0 ? u.d : u.f;
+          const std::vector<Piece>& lst = grp == 0 ? u.d : u.f;
           mdg::DualJob* jobs = grp == 0 ? dd.d : dd.f;
           int32_t tiles = 0;
           for (size_t x = 0; x < lst.size(); ++x) {
-            const size_t i = lst[x];
+            const size_t i = lst[x].call;
             dual_pack(cs[i].plan, w + off, npk == 0 ? P : PX[npk - 1], &jobs[x]);
             npk = (npk + 1) % 3;
             off += prep[i].bytes;
             jobs[x].tile0 = tiles;
-            tiles += jobs[x].tiles_m * jobs[x].tiles_n;
+            jobs[x].tile_begin = lst[x].t0;
+            tiles += lst[x].t1 - lst[x].t0;
             const ExecutionPlan& p = cs[i].plan;
-            (grp == 0 ? flops_d : flops_f) += 2.0 * p.m * p.n * p.k;
+            (grp == 0 ? flops_d : flops_f) += 2.0 * p.m * p.n * p.k * (lst[x].t1 - lst[x].t0) / prep[i].tiles;
           }
           (grp == 0 ? dd.nd : dd.nf) = static_cast<int32_t>(lst.size());
           (grp == 0 ? dd.tiles_d : dd.tiles_f) = tiles;
@@ -582,8 +614,9 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
         dual_launch(dd, flops_d, flops_f, K);
         if (log_units) cuda_check(cudaEventRecord(unit_ev[ui].second, K), "event");
         if (fc)
-          for (const std::vector<size_t>* lst : {&u.d, &u.f})
-            for (size_t i : *lst) fc->add(reference_flops(cs[i].plan));
+          for (const std::vector<Piece>* lst : {&u.d, &u.f})
+            for (const Piece& pc : *lst)
+              if (pc.t1 == prep[pc.call].tiles) fc->add(reference_flops(cs[pc.call].plan));
       }
       k_done[ui] = ev();
       cuda_check(cudaEventRecord(k_done[ui], K), "event");
@@ -625,14 +658,13 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
           float ms = 0;
           cudaEventElapsedTime(&ms, unit_ev[ui].first, unit_ev[ui].second);
           double td = 0, tf = 0, fd = 0, ff = 0;
-          for (size_t i : units[ui].d) {
-            td += est[i];
-            fd += 2.0 * cs[i].plan.m * cs[i].plan.n * cs[i].plan.k;
-          }
-          for (size_t i : units[ui].f) {
-            tf += est[i];
-            ff += 2.0 * cs[i].plan.m * cs[i].plan.n * cs[i].plan.k;
-          }
+          for (int grp = 0; grp < 2; ++grp)
+            for (const Piece& pc : grp == 0 ? units[ui].d : units[ui].f) {
+              const double frac = static_cast<double>(pc.t1 - pc.t0) / prep[pc.call].tiles;
+              const ExecutionPlan& q = cs[pc.call].plan;
+              (grp == 0 ? td : tf) += est[pc.call] * frac;
+              (grp == 0 ? fd : ff) += 2.0 * q.m * q.n * q.k * frac;
+            }
           const double dend = tm[3 * ui + 1] > tm[3 * ui] ? (tm[3 * ui + 1] - tm[3 * ui]) * 1e-6 : 0.0;
           const double fend = tm[3 * ui + 2] > tm[3 * ui] ? (tm[3 * ui + 2] - tm[3 * ui]) * 1e-6 : 0.0;
           std::fprintf(f,

@@ -161,3 +161,35 @@ def test_dual_within_fast_tolerance_of_oracle(monkeypatch):
         assert viol <= 1.0, (p.label, viol)
         err = rel_frobenius(p.C.values(), w.values())
         assert err <= frob_bound(p.label, p.k), (p.label, err)
+
+
+def test_dual_split_tile_ranges(monkeypatch):
+    """A long FP64 call next to short FP32 calls is split into tile ranges over several launches
+    (each launch packs its operands again); the pieces must assemble the single-call result, and
+    calls that depend on the split one (its C read as A) must see all of it."""
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    big = Problem("dddd", 640, 520, 384, seed=1)
+    small = [Problem("cccs" if i % 2 else "ssss", 96, 80, 64, seed=10 + i) for i in range(6)]
+    # a dependent call: reads big's C (640 x 520) as its A
+    dep_b = HostMatrix(M.DT_D, 520, 136).fill(O.orc_rng_state(77, ["b"]))
+    dep_c = HostMatrix(M.DT_D, 640, 136).fill(O.orc_rng_state(77, ["c"]))
+    ref_big, ref_dep = big.C.clone(), dep_c.clone()
+    va, vb, _ = big.views()
+    M.gemm(SCALARS["p7"], va, vb, SCALARS["m3"], ref_big.view(), cfg)
+    M.gemm(SCALARS["one"], ref_big.view(), dep_b.view(), SCALARS["p3"], ref_dep.view(), cfg)
+    ref_small = []
+    for p in small:
+        c = p.C.clone()
+        sa, sb, sc = p.views(C=c)
+        M.gemm(SCALARS["p7"], sa, sb, SCALARS["m3"], sc, cfg)
+        ref_small.append(c)
+    calls = [(SCALARS["p7"], *big.views()[:2], SCALARS["m3"], big.views()[2])]
+    calls += [(SCALARS["p7"], *p.views()[:2], SCALARS["m3"], p.views()[2]) for p in small]
+    calls.append((SCALARS["one"], big.C.view(), dep_b.view(), SCALARS["p3"], dep_c.view()))
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] >= 2, ks
+    assert big.C.buf.tobytes() == ref_big.buf.tobytes()
+    assert dep_c.buf.tobytes() == ref_dep.buf.tobytes()
+    for p, w in zip(small, ref_small):
+        assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
