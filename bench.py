@@ -60,6 +60,10 @@ def parse_args():
     ap.add_argument("--numerics", choices=["fast", "exact"], default="fast")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", choices=["auto", "columns", "chains"], default="auto",
+                    help="multi-GPU split: C/B column panels of every call with A broadcast (columns), or whole "
+                         "calls grouped by the C buffer they update (chains: dependency chains stay on one rank, "
+                         "no collective); auto = chains for the cfg2 sweep, columns otherwise")
     ap.add_argument("--no-serial", action="store_true",
                     help="skip the serialized per-call pass (per-case rates, classic-kernel rooflines); "
                          "for ncu launch lists of the batched step alone")
@@ -198,15 +202,40 @@ def run_b200(args):
     ops = {}
     a_bufs = []
     shard = {}
+    # Multi-GPU split.  chains: every call stays whole; the calls updating one C buffer (a
+    # dependency chain) go to one rank, chains balanced over the ranks by their flops (longest
+    # first); each rank generates the operands it reads.  columns: C and B column panels per
+    # rank, A broadcast from rank 0 inside every step.
+    shard_mode = args.shard if args.shard != "auto" else ("chains" if args.workload == "sweep" else "columns")
+    if world == 1:
+        shard_mode = "columns"
+    mine = set()
+    if shard_mode == "chains":
+        chain_flops = {}
+        for lab, m, n, k, _, _ in items:
+            key = (lab[0], m, n)
+            chain_flops[key] = chain_flops.get(key, 0.0) + M.flops_of_case(M.CaseLabel.parse(lab).case_id(), m, n, k)
+        load = [0.0] * world
+        owner = {}
+        for key in sorted(chain_flops, key=lambda x: -chain_flops[x]):
+            r = min(range(world), key=lambda q: load[q])
+            owner[key] = r
+            load[r] += chain_flops[key]
+        mine = {key for key, r in owner.items() if r == rank}
     for lab, m, n, k, _, _ in items:
-        j0, nb = M.shard_columns(n, world, rank, 128)
+        if shard_mode == "chains":
+            j0, nb = (0, n) if (lab[0], m, n) in mine else (0, 0)
+        else:
+            j0, nb = M.shard_columns(n, world, rank, 128)
         shard[(lab, m, n, k)] = (j0, nb)
+        if nb == 0:
+            continue
         dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
         for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, nb)), ("c", dc, (m, nb))):
             key = (role, dt, shape)
             if key not in ops:
                 t, v = alloc(dt, *shape)
-                tag = f"{args.workload}/{role}/{M.dtype_letter(dt)}/{shape}/r{0 if role == 'a' else rank}"
+                tag = f"{args.workload}/{role}/{M.dtype_letter(dt)}/{shape}/r{0 if role == 'a' or shard_mode == 'chains' else rank}"
                 if dist_kind == "normal":  # normal(0,1) per real component, seeded per operand
                     g = torch.Generator(device=dev).manual_seed(len(ops) * 7919 + 13 * (rank if role != "a" else 0))
                     real = torch.float32 if M.precision_of(dt) == M.SINGLE else torch.float64
@@ -215,13 +244,15 @@ def run_b200(args):
                 else:
                     M.fill_uniform(v, M.Rng(args.seed).split(tag).state, stream)
                 ops[key] = (t, v)
-                if role == "a":
+                if role == "a" and shard_mode == "columns":
                     a_bufs.append(t)
     calls, call_info = [], []  # call_info: (case id, useful flops, computation precision) per call
     for lab, m, n, k, al, be in items:
         j0, nb = shard[(lab, m, n, k)]
         dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
         comp = M.SINGLE if lab[3] == "s" else M.DOUBLE
+        if nb == 0:
+            continue
         va = ops[("a", da, (m, k))][1]
         vb = ops[("b", db, (k, nb))][1]
         vc = ops[("c", dc, (m, nb))][1].with_comp_prec(comp)
@@ -430,7 +461,9 @@ def run_b200(args):
         "data": "synthetic: reference splitmix64 Rng uniform[-1,1) generated on device"
                 if dist_kind == "uniform" else "synthetic: normal(0,1) from a seeded device generator",
         "config": {"workload": desc, "labels": len(items), "numerics": args.numerics,
-                   "parallelism": f"column panels x{world}, A broadcast over NCCL" if world > 1 else "single GPU",
+                   "parallelism": ("single GPU" if world == 1 else
+                                   f"whole calls by C-buffer chain x{world}, chains balanced by flops, no collective"
+                                   if shard_mode == "chains" else f"column panels x{world}, A broadcast over NCCL"),
                    "l2": "operands > L2 per step and a 512 MiB L2 flush between timed steps"},
         "peak_fraction": peak_fraction,
         "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},

@@ -51,10 +51,12 @@ def test_b200_arm_line():
 
 
 @pytest.mark.gpu
-def test_two_rank_path_functional():
-    # two ranks on one GPU with gloo (test hook): exercises sharding, the A
-    # broadcast and the max-over-ranks timing; rank 0 alone prints
+@pytest.mark.parametrize("shard,port", [("columns", 29561), ("chains", 29562)])
+def test_two_rank_path_functional(shard, port):
+    # two ranks on one GPU with gloo (test hook): exercises both splits (column panels with the A
+    # broadcast, whole calls by C-buffer chain) and the max-over-ranks timing; rank 0 alone prints
     d = run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
-             "--master-port", "29561", "bench.py", "--gpus", "2", "--size", "512", "--labels", "dddd,zzzd,cdds",
-             "--steps", "1", "--warmup", "1"], env={"MDGEMM_BENCH_BACKEND": "gloo"})
+             "--master-port", str(port), "bench.py", "--gpus", "2", "--size", "512", "--labels", "dddd,zzzd,cdds,ssss",
+             "--steps", "1", "--warmup", "1", "--shard", shard], env={"MDGEMM_BENCH_BACKEND": "gloo"})
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "strong"
+    assert ("chain" in d["config"]["parallelism"]) == (shard == "chains")
