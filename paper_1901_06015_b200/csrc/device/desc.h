@@ -144,9 +144,12 @@ struct DualDesc {
   int32_t prefetch_c;        // producers warm L2 with each tile's C
   int32_t pad0;
   unsigned long long* timing;  // tuning only: {start min, D end max, F end max} (%globaltimer ns) or null
+  int* counters;               // {D, F} tile counters, zero before the launch (dynamic tiles), or null
   DualJob d[DUAL_MAX_JOBS];
   DualJob f[DUAL_MAX_JOBS];
 };
+// passed by value as a __grid_constant__ kernel parameter (limit 32764 bytes)
+static_assert(sizeof(DualDesc) <= 32000, "DualDesc exceeds the kernel parameter space");
 constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128, DUAL_BK = 16, DUAL_F_BK = 32;
 
 // ---- host launchers (defined in the .cu files) ----

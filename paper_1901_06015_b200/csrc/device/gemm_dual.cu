@@ -35,6 +35,7 @@
 // rounding, same combine.  While one group runs its epilogue the other
 // group's mainloop keeps the SM busy.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -51,7 +52,8 @@ template <int DD_STAGES, int DF_STAGES>
 struct DuRings {
   static constexpr size_t DD_RING = size_t(DD_STAGES) * (DD_SA + DD_SB) * sizeof(double);
   static constexpr size_t DF_RING = size_t(DF_STAGES) * (DF_SA + DF_SB) * sizeof(float);
-  static constexpr size_t SMEM = DD_RING + DF_RING + (2 * DD_STAGES + 2 * DF_STAGES) * sizeof(uint64_t);
+  static constexpr size_t SMEM =
+      DD_RING + DF_RING + (2 * DD_STAGES + 2 * DF_STAGES) * sizeof(uint64_t) + (DD_STAGES + DF_STAGES) * sizeof(int);
 };
 constexpr int DU_THREADS = 512;
 constexpr int DD_WARPS = 8, DF_WARPS = 4;
@@ -273,6 +275,8 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   uint64_t* dempty = dfull + DD_STAGES;
   uint64_t* ffull = dempty + DD_STAGES;
   uint64_t* fempty = ffull + DF_STAGES;
+  int* dslot = reinterpret_cast<int*>(fempty + DF_STAGES);  // tile of each stage's first k-block
+  int* fslot = dslot + DD_STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = static_cast<int>(gridDim.x);
   if (threadIdx.x == 0) {
@@ -292,47 +296,65 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   if (warp >= DD_PROD_WARP) {  // ------------------------------------------ producers
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(RP));
     if (lane != 0) return;
-    if (warp == DD_PROD_WARP) {
+    // Tile order: CTA b starts with tile b; with d.counters every further tile
+    // comes from the group's atomic counter (the tiles are sorted longest-k
+    // first, so CTAs that finish early take the next longest: balanced tails),
+    // else the static boustrophedon rounds.  The producer hands the tile to
+    // its consumers in the first stage's slot; -1 ends the list.
+    auto run_producer = [&](auto* A, auto* B, uint64_t* full, uint64_t* empty, int* slot, const DualJob* jobs,
+                            int njobs, int tiles, int* counter, int STAGES, int BM, int BN, int SA, int SB, int BK,
+                            int esz) {
+      using T = typename std::remove_pointer<decltype(A)>::type;
       int it = 0;
-      for (int r = 0; r * G < d.tiles_d; ++r) {
-        const int v = snake_tile(r, G);
-        if (v >= d.tiles_d) continue;
-        const DualJob& jb = d.d[job_of(d.d, d.nd, v)];
+      auto next = [&](int r) -> int {
+        if (counter) return r == 0 ? static_cast<int>(blockIdx.x) : atomicAdd(counter, 1) + G;
+        int v;
+        do {
+          v = snake_tile(r, G);
+          if (v < tiles) return v;
+          ++r;
+        } while ((r - 1) * G < tiles);
+        return tiles;
+      };
+      for (int r = 0;; ++r) {
+        const int v = next(r);
+        if (v >= tiles) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          slot[s] = -1;
+          mbar_arrive(&full[s]);
+          return;
+        }
+        const DualJob& jb = jobs[job_of(jobs, njobs, v)];
         int tm, tn;
         tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
-        if (d.prefetch_c) prefetch_c(jb, tm, tn, DD_BM, DD_BN);
-        const double* Ag = static_cast<const double*>(jb.a) + static_cast<int64_t>(tm) * DD_BM * jb.lpad;
-        const double* Bg = static_cast<const double*>(jb.b) + static_cast<int64_t>(tn) * DD_BN * jb.lpad;
-        const int nk = static_cast<int>(jb.lpad / DU_BK);
+        if (d.prefetch_c) prefetch_c(jb, tm, tn, BM, BN);
+        const T* Ag = static_cast<const T*>(jb.a) + static_cast<int64_t>(tm) * BM * jb.lpad;
+        const T* Bg = static_cast<const T*>(jb.b) + static_cast<int64_t>(tn) * BN * jb.lpad;
+        const int nk = static_cast<int>(jb.lpad / BK);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % DD_STAGES;
-          if (it >= DD_STAGES) mbar_wait(&dempty[s], ((it / DD_STAGES) - 1) & 1);
-          mbar_arrive_expect_tx(&dfull[s], (DD_SA + DD_SB) * sizeof(double));
-          bulk_g2s(dA + s * DD_SA, Ag + static_cast<int64_t>(kb) * DD_SA, DD_SA * sizeof(double), &dfull[s]);
-          bulk_g2s(dB + s * DD_SB, Bg + static_cast<int64_t>(kb) * DD_SB, DD_SB * sizeof(double), &dfull[s]);
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          if (kb == 0) slot[s] = v;
+          mbar_arrive_expect_tx(&full[s], (SA + SB) * esz);
+          bulk_g2s(A + s * SA, Ag + static_cast<int64_t>(kb) * SA, SA * esz, &full[s]);
+          bulk_g2s(B + s * SB, Bg + static_cast<int64_t>(kb) * SB, SB * esz, &full[s]);
+        }
+        if (!counter && (r + 1) * G >= tiles) {  // static order: done after the last round
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          slot[s] = -1;
+          mbar_arrive(&full[s]);
+          return;
         }
       }
-    } else if (warp == DF_PROD_WARP) {
-      int it = 0;
-      for (int r = 0; r * G < d.tiles_f; ++r) {
-        const int v = snake_tile(r, G);
-        if (v >= d.tiles_f) continue;
-        const DualJob& jb = d.f[job_of(d.f, d.nf, v)];
-        int tm, tn;
-        tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
-        if (d.prefetch_c) prefetch_c(jb, tm, tn, DF_BM, DF_BN);
-        const float* Ag = static_cast<const float*>(jb.a) + static_cast<int64_t>(tm) * DF_BM * jb.lpad;
-        const float* Bg = static_cast<const float*>(jb.b) + static_cast<int64_t>(tn) * DF_BN * jb.lpad;
-        const int nk = static_cast<int>(jb.lpad / DF_BK);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % DF_STAGES;
-          if (it >= DF_STAGES) mbar_wait(&fempty[s], ((it / DF_STAGES) - 1) & 1);
-          mbar_arrive_expect_tx(&ffull[s], (DF_SA + DF_SB) * sizeof(float));
-          bulk_g2s(fA + s * DF_SA, Ag + static_cast<int64_t>(kb) * DF_SA, DF_SA * sizeof(float), &ffull[s]);
-          bulk_g2s(fB + s * DF_SB, Bg + static_cast<int64_t>(kb) * DF_SB, DF_SB * sizeof(float), &ffull[s]);
-        }
-      }
-    }
+    };
+    if (warp == DD_PROD_WARP)
+      run_producer(dA, dB, dfull, dempty, dslot, d.d, d.nd, d.tiles_d, d.counters ? d.counters : nullptr, DD_STAGES,
+                   DD_BM, DD_BN, DD_SA, DD_SB, DU_BK, static_cast<int>(sizeof(double)));
+    else if (warp == DF_PROD_WARP)
+      run_producer(fA, fB, ffull, fempty, fslot, d.f, d.nf, d.tiles_f, d.counters ? d.counters + 1 : nullptr,
+                   DF_STAGES, DF_BM, DF_BN, DF_SA, DF_SB, DF_BK, static_cast<int>(sizeof(float)));
     return;
   }
 
@@ -344,16 +366,16 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     const double* b_base = dB + wn * 32 + g + tig * DD_BN;
     const uint32_t full_u = smem_u32(dfull), empty_u = smem_u32(dempty);
     int it = 0;
-    for (int r = 0; r * G < d.tiles_d; ++r) {
-        const int v = snake_tile(r, G);
-        if (v >= d.tiles_d) continue;
-      const int jx = job_of(d.d, d.nd, v);
-      int tm, tn;
-      {
-        const DualJob& jb = d.d[jx];
-        tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+    for (;;) {
+      {  // the producer names the next tile in its first stage's slot
+        const int s0 = it % DD_STAGES;
+        mbar_wait_u32(full_u + 8 * s0, (it / DD_STAGES) & 1);
       }
-      const int nk = static_cast<int>(d.d[jx].lpad / DU_BK);
+      int v = *reinterpret_cast<volatile int*>(&dslot[it % DD_STAGES]);
+      if (v < 0) break;
+      // only v stays live through the mainloop (the group runs at its register
+      // cap); the job and tile coordinates are derived again for the epilogue
+      const int nk = static_cast<int>(d.d[job_of(d.d, d.nd, v)].lpad / DU_BK);
       double acc[8][4][2];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
@@ -361,7 +383,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % DD_STAGES;
-        mbar_wait_u32(full_u + 8 * s, (it / DD_STAGES) & 1);
+        if (kb > 0) mbar_wait_u32(full_u + 8 * s, (it / DD_STAGES) & 1);
         const double* a = a_base + s * DD_SA;
         const double* b = b_base + s * DD_SB;
 #pragma unroll
@@ -380,9 +402,11 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
       }
-      // the job's parameters are re-read after the mainloop (register cap)
+      asm volatile("" : "+r"(v));
+      const int jx = job_of(d.d, d.nd, v);
       const DualJob* jp = &d.d[jx];
-      asm volatile("" : "+l"(jp));
+      int tm, tn;
+      tile_coords(jp->tile_begin + v - jp->tile0, jp->tiles_m, jp->tiles_n, 0, tm, tn);
       MDG_DISPATCH_CDT(jp->out.dtype, CDT, { epilogue_d<CDT>(*jp, tm, tn, wm, wn, lane, acc); });
     }
     if (d.timing && lane == 0) atomicMax(&d.timing[1], globaltimer());
@@ -397,16 +421,14 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   const float* b_base = fB + tx * 4;
   const uint32_t full_u = smem_u32(ffull), empty_u = smem_u32(fempty);
   int it = 0;
-  for (int r = 0; r * G < d.tiles_f; ++r) {
-        const int v = snake_tile(r, G);
-        if (v >= d.tiles_f) continue;
-    const int jx = job_of(d.f, d.nf, v);
-    int tm, tn;
+  for (;;) {
     {
-      const DualJob& jb = d.f[jx];
-      tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+      const int s0 = it % DF_STAGES;
+      mbar_wait_u32(full_u + 8 * s0, (it / DF_STAGES) & 1);
     }
-    const int nk = static_cast<int>(d.f[jx].lpad / DF_BK);
+    int v = *reinterpret_cast<volatile int*>(&fslot[it % DF_STAGES]);
+    if (v < 0) break;
+    const int nk = static_cast<int>(d.f[job_of(d.f, d.nf, v)].lpad / DF_BK);
     uint64_t acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
@@ -414,7 +436,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
     for (int kb = 0; kb < nk; ++kb, ++it) {
       const int s = it % DF_STAGES;
-      mbar_wait_u32(full_u + 8 * s, (it / DF_STAGES) & 1);
+      if (kb > 0) mbar_wait_u32(full_u + 8 * s, (it / DF_STAGES) & 1);
       const float* a = a_base + s * DF_SA;
       const float* b = b_base + s * DF_SB;
 #pragma unroll
@@ -437,8 +459,10 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       __syncwarp();
       if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
     }
-    const DualJob* jp = &d.f[jx];
-    asm volatile("" : "+l"(jp));
+    asm volatile("" : "+r"(v));
+    const DualJob* jp = &d.f[job_of(d.f, d.nf, v)];
+    int tm, tn;
+    tile_coords(jp->tile_begin + v - jp->tile0, jp->tiles_m, jp->tiles_n, 0, tm, tn);
     MDG_DISPATCH_CDT(jp->out.dtype, CDT, { epilogue_f<CDT>(*jp, tm, tn, ty, tx, acc); });
   }
   if (d.timing && lane == 0) atomicMax(&d.timing[2], globaltimer());

@@ -27,9 +27,10 @@ def _batch_with_profile(calls, cfg):
     return M.profile_end()
 
 
-@pytest.mark.parametrize("c_kind", ["col", "row"])
-def test_dual_all_labels_equal_single_calls(monkeypatch, c_kind):
+@pytest.mark.parametrize("c_kind,dynamic", [("col", "0"), ("row", "0"), ("col", "1")])
+def test_dual_all_labels_equal_single_calls(monkeypatch, c_kind, dynamic):
     monkeypatch.setenv("MDGEMM_DUAL", "1")
+    monkeypatch.setenv("MDGEMM_DUAL_DYNAMIC", dynamic)  # static tile order, or the atomic-counter one
     cfg = config({"gpu.numerics": "fast"})
     probs = [Problem(l, *SHAPES[i % len(SHAPES)], c_kind=c_kind, seed=7 + i, trans_a=(i % 5 == 3))
              for i, l in enumerate(LABELS)]
