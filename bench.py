@@ -335,6 +335,29 @@ def run_b200(args):
         c["ideal_ms"] += fl / ((pk0["ffma_tflops"] if comp == "s" else pk0["dmma_tflops"]) * 1e9)
     per_case = {name: {"calls": c["calls"], "GFLOPS": round(c["flops"] / c["ms"] / 1e6, 1),
                        "frac_of_peak": round(c["ideal_ms"] / c["ms"], 3)} for name, c in per_case.items()}
+    # Per mixed-datatype case, batched (the way the timed step runs them): the calls of one case
+    # as one gemm_batch (FP64 and FP32 labels of the case share the dual-pipe launches)
+    per_case_batched = {}
+    if not args.no_serial and args.workload == "sweep":
+        pk1 = peaks()
+        by_case = {}
+        for (cid, fl, comp), call in zip(call_info, calls):
+            e = by_case.setdefault(M.CASE_NAMES[cid], {"calls": [], "flops": 0.0, "ideal_ms": 0.0})
+            e["calls"].append(call)
+            e["flops"] += fl
+            e["ideal_ms"] += fl / ((pk1["ffma_tflops"] if comp == "s" else pk1["dmma_tflops"]) * 1e9)
+        for name, e in by_case.items():
+            M.gemm_batch(e["calls"], cfg, stream=stream, sync=False)  # warm-up
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            M.gemm_batch(e["calls"], cfg, stream=stream, sync=False)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            per_case_batched[name] = {"calls": len(e["calls"]), "GFLOPS": round(e["flops"] / ms / 1e6, 1),
+                                      "frac_of_serialized_peak": round(e["ideal_ms"] / ms, 3)}
     if world > 1:
         t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -473,6 +496,7 @@ def run_b200(args):
                          if v["launches"] or v["ms"]},
         "kernels": kernels,
         "per_case": per_case,
+        "per_case_batched": per_case_batched,
         "serialized_step_ms": serial_ms,
         "step_ms": [round(x, 3) for x in step_ms],
         "host_enqueue_ms": [round(x, 1) for x in enqueue_ms],
