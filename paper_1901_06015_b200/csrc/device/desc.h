@@ -34,11 +34,17 @@ struct DEpilogue {
   // type, outer: columns) for TMA tensor loads/stores of C_BOX_COLS-column
   // boxes; valid when cmap_ok (column-major C with 16-byte aligned columns).
   CUtensorMap cmap;
+  // The same C as SWIZZLE_128B boxes of 128 bytes x C_BOX_COLS lines (real
+  // column-major C only, sw_ok): the warp-specialised kernels' tile buffer then
+  // has no shared-memory bank conflicts in the combine pass.
+  CUtensorMap cmap_sw;
   DView out;
   int32_t pair;
   int32_t cmap_ok;
   DBeta beta;
   int64_t me, ne;
+  int32_t sw_ok;
+  int32_t pad_sw;
 };
 constexpr int C_BOX_COLS = 16;  // lines (columns, or rows for MDG_CMAP_ROWS) per TMA box
 // DEpilogue::cmap_ok: how the tensor map covers C

@@ -30,6 +30,7 @@
 // 16-byte aligned C (a TMA tensor map, d.epi.cmap_ok); the driver keeps the
 // classic kernel otherwise.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -104,6 +105,24 @@ __device__ __forceinline__ Seg ws_seg(const WsSched& s, int idx) {
   }
   if (idx < s.full1 - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
   return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
+}
+
+// Byte offset of element (r, c) of the 128x128 C tile when it is held as
+// SWIZZLE_128B boxes of 128 bytes (128/ESZ rows) x 16 columns, column-chunk
+// major: inside a box, column cc is one 128-byte line whose 16-byte chunks are
+// permuted by XOR with cc % 8 (the TMA 128B swizzle of a 1 KB-aligned box).
+// accumulate_element for real C in its storage precision (combine_typed's real path)
+__device__ __forceinline__ float ws_add(float x, float y) { return __fadd_rn(x, y); }
+__device__ __forceinline__ double ws_add(double x, double y) { return __dadd_rn(x, y); }
+__device__ __forceinline__ float ws_mul(float x, float y) { return __fmul_rn(x, y); }
+__device__ __forceinline__ double ws_mul(double x, double y) { return __dmul_rn(x, y); }
+
+template <int ESZ>
+__device__ __forceinline__ uint32_t ws_swz_off(int r, int c) {
+  constexpr int RB = 128 / ESZ, NRB = 128 / RB;
+  const int cb = c >> 4, cc = c & 15, rb = r / RB, rr = r % RB;
+  const uint32_t byte = static_cast<uint32_t>(rr * ESZ);
+  return static_cast<uint32_t>((cb * NRB + rb) * 2048 + cc * 128) + ((((byte >> 4) ^ (cc & 7)) << 4) | (byte & 15));
 }
 
 __device__ __forceinline__ void dmma884_ws(double& c0, double& c1, double a, double b) {
@@ -183,6 +202,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       x0 = (prow ? tm * (WS_BM / 2) : tm * WS_BM) * NC;
       y0 = pcol ? tn * (WS_BN / 2) : tn * WS_BN;
     };
+    // swizzled layout (e.sw_ok, real C): 128-byte x 16-column boxes, column
+    // chunk major, SWIZZLE_128B (ws_swz_off); else one box per 16 columns
+    const bool swz = NC == 1 && e.sw_ok && (smem_u32(ctile) & 1023) == 0;  // the swizzle atom is 1 KB
+    constexpr int RB = 128 / O::ESZ, NRB = WS_BM / RB;
     auto load = [&](const Seg& sg) {  // C of the tile the MMA warps finish next
       if (!reads_c) {
         mbar_arrive(c_full);
@@ -191,8 +214,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       int x0, y0;
       coords(sg, x0, y0);
       mbar_arrive_expect_tx(c_full, tile_bytes);
+      if (swz) {
+        for (int b = 0; b < WS_BN / C_BOX_COLS; ++b)
+          for (int rb = 0; rb < NRB; ++rb)
+            tensor_load_2d(ctile + static_cast<size_t>(b * NRB + rb) * 2048, &e.cmap_sw, x0 + rb * RB,
+                           y0 + b * C_BOX_COLS, c_full);
+        return;
+      }
       for (int b = 0; b < ocols; b += C_BOX_COLS)
         tensor_load_2d(ctile + static_cast<size_t>(b) * col_bytes, &e.cmap, x0, y0 + b, c_full);
+    };
+    auto store = [&](int x0, int y0) {
+      if (swz) {
+        for (int b = 0; b < WS_BN / C_BOX_COLS; ++b)
+          for (int rb = 0; rb < NRB; ++rb)
+            tensor_store_2d(&e.cmap_sw, x0 + rb * RB, y0 + b * C_BOX_COLS,
+                            ctile + static_cast<size_t>(b * NRB + rb) * 2048);
+        return;
+      }
+      for (int b = 0; b < ocols; b += C_BOX_COLS)
+        tensor_store_2d(&e.cmap, x0, y0 + b, ctile + static_cast<size_t>(b) * col_bytes);
     };
     int epis = 0, pending = -1;  // pending: segment whose C is loaded and whose results are awaited
     for (int si = 0; si < sc.nseg; ++si) {
@@ -202,8 +243,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
         mbar_wait(res_full, epis & 1);
         int x0, y0;
         coords(ws_seg(sc, pending), x0, y0);
-        for (int b = 0; b < ocols; b += C_BOX_COLS)
-          tensor_store_2d(&e.cmap, x0, y0 + b, ctile + static_cast<size_t>(b) * col_bytes);
+        store(x0, y0);
         bulk_commit();
         bulk_wait_read();
         ++epis;
@@ -216,8 +256,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       mbar_wait(res_full, epis & 1);
       int x0, y0;
       coords(ws_seg(sc, pending), x0, y0);
-      for (int b = 0; b < ocols; b += C_BOX_COLS)
-        tensor_store_2d(&e.cmap, x0, y0 + b, ctile + static_cast<size_t>(b) * col_bytes);
+      store(x0, y0);
       bulk_commit();
       bulk_wait_read();  // the smem must outlive the store's reads
     }
@@ -296,24 +335,54 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
     asm volatile("" : "+l"(ep));
     const bool eprow = ep->pair == MDG_PAIR_ROWS, epcol = ep->pair == MDG_PAIR_COLS;
     const int eorows = eprow ? WS_BM / 2 : WS_BM;
-    const bool ereads = !ep->beta.is_zero, econj = ep->out.conj != 0;
+    const DBeta eb = ep->beta;  // one copy in registers, not a parameter-space load per element
+    const bool ereads = !eb.is_zero, econj = ep->out.conj != 0;
+    const bool eswz = NC == 1 && ep->sw_ok && (smem_u32(smem + W::RING) & 1023) == 0;
     R* const ect = reinterpret_cast<R*>(smem + W::RING);
+    if constexpr (NC == 1) {
+      // real C: accumulate_element (combine_typed) with the beta case and the
+      // tile layout resolved once per tile, not per element
+      const R rb = static_cast<R>(eb.re);
+      auto pass = [&](auto mode, auto swz) {
+#pragma unroll
+        for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+          for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int r = wm * 64 + i * 8 + g, c = wn * 32 + j * 8 + 2 * tig + h;
+              R* p = decltype(swz)::value ? reinterpret_cast<R*>(smem + W::RING + ws_swz_off<O::ESZ>(r, c))
+                                          : ect + c * eorows + r;
+              const R tv = static_cast<R>(acc[i][j][h]);
+              if constexpr (decltype(mode)::value == 0) {
+                *p = tv;
+              } else if constexpr (decltype(mode)::value == 1) {
+                *p = ws_add(*p, tv);
+              } else {
+                *p = ws_add(ws_mul(rb, *p), tv);
+              }
+            }
+      };
+      using Z = std::integral_constant<int, 0>;
+      using One = std::integral_constant<int, 1>;
+      using Gen = std::integral_constant<int, 2>;
+      if (eswz) {
+        if (eb.is_zero) pass(Z{}, std::true_type{});
+        else if (eb.is_one) pass(One{}, std::true_type{});
+        else pass(Gen{}, std::true_type{});
+      } else {
+        if (eb.is_zero) pass(Z{}, std::false_type{});
+        else if (eb.is_one) pass(One{}, std::false_type{});
+        else pass(Gen{}, std::false_type{});
+      }
+    } else {
 #pragma unroll
     for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
       for (int j = 0; j < WS_NT; ++j) {
         const int r = wm * 64 + i * 8 + g, c = wn * 32 + j * 8 + 2 * tig;
         const double a0 = acc[i][j][0], a1 = acc[i][j][1];  // (r, c), (r, c + 1)
-        if constexpr (NC == 1) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            R* p = ect + (c + h) * eorows + r;
-            R cv = ereads ? *p : R(0);
-            const R tv = static_cast<R>(h ? a1 : a0);
-            combine_typed<CDT>(ep->beta, econj, &cv, &tv);
-            *p = cv;
-          }
-        } else {
+        {
           // complex C: a column pair (pcol: re, im of element (r, c/2)) or a
           // row pair held by lanes g and g^1 (prow: element (r/2, c) for even
           // g, (r/2, c+1) for odd g after one exchange)
@@ -335,11 +404,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
             cv[0] = p[0];
             cv[1] = p[1];
           }
-          combine_typed<CDT>(ep->beta, econj, cv, tv);
+          combine_typed<CDT>(eb, econj, cv, tv);
           p[0] = cv[0];
           p[1] = cv[1];
         }
       }
+    }
     fence_proxy_async();  // generic writes of ctile before the C mover's TMA store reads them
     __syncwarp();
     if (lane == 0) mbar_arrive(res_full);

@@ -262,6 +262,18 @@ static int encode_c_map(mdg::DEpilogue& e, int bm, int bn) {
                          e.out.base, dims, strides, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  e.sw_ok = 0;
+  if (ok && mode == mdg::MDG_CMAP_COLS && nc == 1) {  // swizzled 128-byte boxes (warp-specialised kernels)
+    const cuuint32_t box_sw[2] = {static_cast<cuuint32_t>(128 / esr), static_cast<cuuint32_t>(mdg::C_BOX_COLS)};
+    e.sw_ok = encode(&e.cmap_sw, single ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                     e.out.base, dims, strides, box_sw, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+                  ? 1
+                  : 0;
+    if (const char* f = std::getenv("MDGEMM_C_SWIZZLE"))  // tuning: 0 = plain boxes in the WS kernels
+      if (std::atoi(f) == 0) e.sw_ok = 0;
+  }
   return ok ? mode : mdg::MDG_CMAP_NONE;
 }
 
