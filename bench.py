@@ -27,6 +27,7 @@ Arms:
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -117,6 +118,8 @@ def useful_flops(items):
 
 
 # ------------------------------------------------------------------- clocks
+# nvidia-smi's NVML queries hold the driver lock: at a 200 ms period they stalled the host
+# enqueue of lone calls by 15-65 ms in 2 of 10 steps (cfg3 33.1 -> 35.3 TFLOP/s at 1000 ms)
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -127,7 +130,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(device_index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=self.file, stderr=subprocess.DEVNULL)
+                 "-lms", os.environ.get("MDGEMM_BENCH_CLOCK_MS", "1000")], stdout=self.file, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
@@ -275,6 +278,10 @@ def run_b200(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # no cyclic-GC pass in the middle of the timed steps (a full collection of a process with torch
+    # loaded stalls the host enqueue for tens of ms; lone calls then leave the GPU idle)
+    gc.collect()
+    gc.disable()
     sampler = ClockSampler(local)
     launches0 = M.launch_count()
     step_ms, enqueue_ms = [], []
@@ -291,6 +298,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     launches = M.launch_count() - launches0
     clocks = sampler.stop()
+    gc.enable()
     total_ms = sum(step_ms)
 
     # Kernels of the timed step itself: one more step of the same batch with the
@@ -456,11 +464,14 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
         s0 = M.staging_bytes()
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             M.gemm_batch(hcalls, cfg)
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
+        gc.enable()
         s1 = M.staging_bytes()
         h2d = (s1[0] - s0[0]) // args.steps
         d2h = (s1[1] - s0[1]) // args.steps

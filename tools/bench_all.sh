@@ -2,7 +2,7 @@
 # Every BASELINE.json config through bench.py on one GPU (device-resident value + roofline).
 mkdir -p gpurun_out/all
 for w in cfg1 cfg3 cfg4-cdds cfg4-szzs cfg4-zczd cfg5-k64 cfg5-k256 cfg5-k1024; do
-  timeout 600 python bench.py --workload $w --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/all/$w.json 2> gpurun_out/all/$w.err
+  timeout 600 python bench.py --workload $w --steps 10 --warmup 5 --no-e2e --no-cpu > gpurun_out/all/$w.json 2> gpurun_out/all/$w.err
   python - "$w" <<'PY'
 import json, sys
 w = sys.argv[1]
