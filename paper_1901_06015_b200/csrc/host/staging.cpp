@@ -206,14 +206,30 @@ int dual_mode() {
   return f ? std::atoi(f) : 1;
 }
 
+// Everything the host decides about a dual-pipe batch before any device work.
+struct DualPlan {
+  std::vector<int> kind;          // per call: 0 through execute(), 1 FP64 (D) job, 2 FP32 (F) job
+  std::vector<DualPrep> prep;     // pack geometry of the dual jobs
+  std::vector<double> est;        // estimated device time of a whole call at the co-run rate
+  std::vector<long> ab_writer;    // latest call writing what this call's A/B read (its packs wait for it)
+  std::vector<Unit> units;        // the launches, in order
+  std::vector<long> unit_of;      // last launch holding a piece of the call
+  std::vector<long> first_unit;   // first one
+  std::vector<Window> all;        // distinct host windows (each becomes one resident copy)
+  size_t host_bytes = 0;
+  size_t arena_bytes = 0;         // largest launch's packed operands
+};
+
 }  // namespace
 
-bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
-                  cudaStream_t user, bool sync, FlopCounter* fc) {
+// Dependency DAG (device-memory conflicts) + list schedule into launches.
+// Host only; false when the batch is not for the dual kernel.
+bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
   const int mode = dual_mode();
   const size_t n = cs.size();
   if (mode == 0 || n < 2 || cfg.numerics != Numerics::Fast) return false;
-  std::vector<int> kind(n, 0);  // 0 classic, 1 D, 2 F
+  P.kind.assign(n, 0);
+  std::vector<int>& kind = P.kind;
   size_t nd = 0, nf = 0;
   for (size_t i = 0; i < n; ++i)
     if (dual_eligible(cs[i].plan, cfg.numerics)) {
@@ -225,7 +241,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
 
   // ---- host windows: per-call hulls; any two overlapping hulls must be identical
   std::vector<std::vector<Window>> hulls(n);
-  std::vector<Window> all;
+  std::vector<Window>& all = P.all;
   for (size_t i = 0; i < n; ++i) {
     std::vector<Window>& hs = hulls[i];
     for (int r = 0; r < 3; ++r)
@@ -247,7 +263,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   });
   all.erase(std::unique(all.begin(), all.end(), [](const Window& a, const Window& b) { return a.lo == b.lo && a.hi == b.hi; }),
             all.end());
-  size_t host_bytes = 0;
+  size_t& host_bytes = P.host_bytes;
   for (size_t x = 0; x < all.size(); ++x) {
     host_bytes += all[x].bytes();
     if (x + 1 < all.size() && all[x].overlaps(all[x + 1])) return false;
@@ -272,7 +288,8 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
   std::vector<WinState> ws;
   std::vector<std::vector<long>> succ(n);
   std::vector<int> npred(n, 0);
-  std::vector<long> ab_writer(n, -1);  // latest call writing what this call's A/B read (packs wait for it)
+  P.ab_writer.assign(n, -1);
+  std::vector<long>& ab_writer = P.ab_writer;
   for (size_t i = 0; i < n; ++i) {
     const Call& c = cs[i];
     std::vector<long> preds;
@@ -320,8 +337,10 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       rate_f = b * 1e12;
     }
   }
-  std::vector<DualPrep> prep(n);
-  std::vector<double> est(n, 0.0);
+  P.prep.assign(n, DualPrep{});
+  P.est.assign(n, 0.0);
+  std::vector<DualPrep>& prep = P.prep;
+  std::vector<double>& est = P.est;
   size_t max_call_bytes = 0;
   for (size_t i = 0; i < n; ++i)
     if (kind[i]) {
@@ -339,9 +358,11 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     tail[i] = t + (kind[i] ? est[i] : 1e-5);
   }
   auto by_priority = [&](size_t x, size_t y) { return tail[x] != tail[y] ? tail[x] > tail[y] : x < y; };
-  std::vector<Unit> units;
-  std::vector<long> unit_of(n, -1);     // last launch holding a piece of the call
-  std::vector<long> first_unit(n, -1);  // first one
+  std::vector<Unit>& units = P.units;
+  P.unit_of.assign(n, -1);
+  P.first_unit.assign(n, -1);
+  std::vector<long>& unit_of = P.unit_of;
+  std::vector<long>& first_unit = P.first_unit;
   std::vector<int32_t> next_tile(n, 0);
   auto rem_est = [&](size_t i) {
     return est[i] * static_cast<double>(prep[i].tiles - next_tile[i]) / static_cast<double>(prep[i].tiles);
@@ -426,7 +447,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     std::stable_sort(u.f.begin(), u.f.end(), by_k);
     units.push_back(std::move(u));
   }
-  size_t arena_bytes = 0;
+  size_t& arena_bytes = P.arena_bytes;
   for (const Unit& u : units) arena_bytes = std::max(arena_bytes, u.bytes);
   if (const char* logp = std::getenv("MDGEMM_DUAL_LOG")) {  // tuning: the launch schedule
     if (FILE* f = std::fopen(logp, "a")) {
@@ -441,11 +462,21 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
       std::fclose(f);
     }
   }
-  const size_t budget = reserve_for_batch(host_bytes, arena_bytes, 2);
-  if (host_bytes > budget) {  // does not fit: the stream scheduler evicts as it goes
-    for (Call& c : cs) c.dev_read[0] = c.dev_read[1] = c.dev_write = Window{};
-    return false;
-  }
+  return true;
+}
+
+// Issue a scheduled dual batch: host copies, packs, launches, write-backs.
+void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const DualPlan& plan, cudaStream_t user,
+               bool sync, FlopCounter* fc) {
+  const size_t n = cs.size();
+  const std::vector<DualPrep>& prep = plan.prep;
+  const std::vector<double>& est = plan.est;
+  const std::vector<long>& ab_writer = plan.ab_writer;
+  const std::vector<Unit>& units = plan.units;
+  const std::vector<long>& unit_of = plan.unit_of;
+  const std::vector<long>& first_unit = plan.first_unit;
+  const std::vector<Window>& all = plan.all;
+  const size_t arena_bytes = plan.arena_bytes;
 
   // ---- emission
   // K: the dual launches (and classic units) in order; P: packs, fanned out to
@@ -700,6 +731,18 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S,
     throw;
   }
   cleanup(failed);
+}
+
+bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S, cudaStream_t user, bool sync,
+                  FlopCounter* fc) {
+  DualPlan plan;
+  if (!dual_schedule(cs, cfg, plan)) return false;
+  const size_t budget = reserve_for_batch(plan.host_bytes, plan.arena_bytes, 2);
+  if (plan.host_bytes > budget) {  // does not fit: the stream scheduler evicts as it goes
+    for (Call& c : cs) c.dev_read[0] = c.dev_read[1] = c.dev_write = Window{};
+    return false;
+  }
+  dual_emit(cs, cfg, S, plan, user, sync, fc);
   return true;
 }
 
