@@ -494,7 +494,8 @@ def run_b200(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (per label computation precision)",
         "data": "synthetic: reference splitmix64 Rng uniform[-1,1) generated on device"
                 if dist_kind == "uniform" else "synthetic: normal(0,1) from a seeded device generator",
-        "config": {"workload": desc, "labels": len(items), "numerics": args.numerics,
+        "config": {"workload": desc, "calls": len(items), "labels": len({it[0] for it in items}),
+                   "numerics": args.numerics,
                    "parallelism": ("single GPU" if world == 1 else
                                    f"whole calls by C-buffer chain x{world}, chains balanced by flops, no collective"
                                    if shard_mode == "chains" else f"column panels x{world}, A broadcast over NCCL"),
@@ -502,7 +503,9 @@ def run_b200(args):
         "peak_fraction": peak_fraction,
         "peaks": {"dmma_tflops": pk["dmma_tflops"], "ffma_tflops": pk["ffma_tflops"]},
         "roofline": roof,
-        "kernel_share": kernel_share,
+        "kernel_share": kernel_share,  # serialized pass of lone calls (classic kernels)
+        "step_kernel_share": ({"dual": round(dual["ms"] / (total_ms / args.steps), 4)}
+                              if dual.get("launches", 0) else None),
         "step_kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3)} for k, v in bstats.items()
                          if v["launches"] or v["ms"]},
         "kernels": kernels,
