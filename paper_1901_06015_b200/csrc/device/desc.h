@@ -149,7 +149,7 @@ struct DualDesc {
   int32_t tiles_d, tiles_f;  // virtual tiles per group
   int32_t prefetch_c;        // producers warm L2 with each tile's C
   int32_t pad0;
-  unsigned long long* timing;  // tuning only: {start min, D end max, F end max} (%globaltimer ns) or null
+  unsigned long long* timing;  // tuning only: {~first start, D end, F end} (%globaltimer ns, max-reduced) or null
   int* counters;               // {D, F} tile counters, zero before the launch (dynamic tiles), or null
   DualJob d[DUAL_MAX_JOBS];
   DualJob f[DUAL_MAX_JOBS];

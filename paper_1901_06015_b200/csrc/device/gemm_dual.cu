@@ -289,7 +289,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       mbar_init(&fempty[s], DF_WARPS);
     }
     mbar_fence_init();
-    if (d.timing) atomicMin(&d.timing[0], globaltimer());
+    if (d.timing) atomicMax(&d.timing[0], ~globaltimer());  // ~start: zero-initialised like the ends
   }
   __syncthreads();
 
