@@ -36,7 +36,9 @@ template <int CDT>
 struct FwCfg {
   using O = OutType<CDT>;
   static constexpr int ESZR = O::kSingle ? 4 : 8;
-  static constexpr size_t CTILE = size_t(FW_BM) * FW_BN * ESZR;  // 64 / 128 KB
+  // 128 KB: double C, or single C held as the real part of an interleaved
+  // complex C (the imaginary halves ride along unchanged)
+  static constexpr size_t CTILE = size_t(FW_BM) * FW_BN * 8;
   static constexpr int STAGES = O::kSingle ? 6 : 4;              // 96 / 64 KB ring
   static constexpr size_t RING = size_t(STAGES) * (FW_STAGE_A + FW_STAGE_B) * sizeof(float);
   static constexpr size_t SMEM = RING + CTILE + (2 * STAGES + 2) * sizeof(uint64_t);
@@ -150,12 +152,13 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
 
   if (warp == FW_CMOV_WARP) {  // ------------------------------------------ C mover
     if (lane != 0) return;
-    const uint32_t col_bytes = orows * O::ESZ;
+    const bool halfc = NC == 1 && e.cmap_ok == MDG_CMAP_REAL_PART;  // real part of interleaved complex C
+    const uint32_t col_bytes = (halfc ? 2 : 1) * orows * O::ESZ;
     const uint32_t tile_bytes = static_cast<uint32_t>(ocols) * col_bytes;
     auto coords = [&](const Seg& sg, int& x0, int& y0) {
       int tm, tn;
       tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
-      x0 = (prow ? tm * (FW_BM / 2) : tm * FW_BM) * NC;
+      x0 = (prow ? tm * (FW_BM / 2) : tm * FW_BM) * (halfc ? 2 : NC);
       y0 = pcol ? tn * (FW_BN / 2) : tn * FW_BN;
     };
     auto store = [&](int seg_idx) {
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
         ++epis;
       }
       fence_proxy_async();
-      if (reads_c) {
+      if (reads_c || halfc) {  // a real part always needs the imaginary halves it writes back
         int x0, y0;
         coords(sg, x0, y0);
         mbar_arrive_expect_tx(c_full, tile_bytes);
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
     }
     // combine with this tile's C (already in ctile) in place
     mbar_wait(c_full, epis & 1);
+    const bool e_half = NC == 1 && e.cmap_ok == MDG_CMAP_REAL_PART;
     auto val = [&](int i, int j) -> float {
       const uint64_t v = acc[i][j >> 1];
       return __uint_as_float(static_cast<uint32_t>((j & 1) ? (v >> 32) : v));
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
       for (int j = 0; j < 8; ++j) {
         const int c = j < 4 ? tx * 4 + j : FW_BN / 2 + tx * 4 + (j - 4);
         if constexpr (NC == 1) {
-          R* p = ct + c * orows + r;
+          R* p = e_half ? ct + (c * orows + r) * 2 : ct + c * orows + r;
           R cv = reads_c ? *p : R(0);
           const R tv = static_cast<R>(val(i, j));
           combine_typed<CDT>(e.beta, conj, &cv, &tv);

@@ -350,8 +350,11 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     probe.out = to_dview(p.c);
     probe.pair = static_cast<int32_t>(p.pair_axis);
     const bool complex_c = probe.out.dtype == MDG_DT_C || probe.out.dtype == MDG_DT_Z;
-    const bool c_ok = encode_c_map(probe, 128, 128) == mdg::MDG_CMAP_COLS &&  // WS kernels: column-major C
-                      (!complex_c || probe.pair != MDG_PAIR_NONE);
+    const int cmode = encode_c_map(probe, 128, 128);
+    // WS kernels: column-major C; the FFMA one also the real part of an
+    // interleaved complex C (case 1c: cfg4 cdds)
+    const bool c_ok = (cmode == mdg::MDG_CMAP_COLS && (!complex_c || probe.pair != MDG_PAIR_NONE)) ||
+                      (single && cmode == mdg::MDG_CMAP_REAL_PART && probe.out.dtype == MDG_DT_S);
     // auto: real C (measured at the cfg2 sizes 2048-4096: DMMA +1..7 %,
     // FFMA +2..4 %, short k far more -- rank-64 ssss 19.6 -> 27.3 TFLOP/s;
     // complex C -1..2 %), one full wave of 128x128 tiles,

@@ -52,7 +52,8 @@ def test_ws_against_oracle(beta, monkeypatch):
     assert O.orc_violation(SCALARS["p7"], va, vb, SCALARS[beta], vc, va_after, p.comp) <= 1.0
 
 
-@pytest.mark.parametrize("label", ["ssss", "dsss", "cccs", "cdzs", "zdzs", "szzs", "sdds", "csds"])
+@pytest.mark.parametrize("label", ["ssss", "dsss", "cccs", "cdzs", "zdzs", "szzs", "sdds", "csds",
+                                   "cdds", "csss", "zdds"])  # 1c: the real part of a complex C
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("streamk", ["0", "-1"])
 def test_ffma_ws_bitwise_equals_classic(label, shape, streamk, monkeypatch):
