@@ -194,3 +194,23 @@ def test_dual_split_tile_ranges(monkeypatch):
     assert dep_c.buf.tobytes() == ref_dep.buf.tobytes()
     for p, w in zip(small, ref_small):
         assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
+
+
+def test_dual_many_small_calls(monkeypatch):
+    """More independent calls than one launch's job lists hold (DUAL_MAX_JOBS per group): the
+    schedule spreads them over several launches; every call bitwise equal to its single call."""
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = config({"gpu.numerics": "fast"})
+    labels = ["dddd", "ssss", "zzzd", "cccs", "dssd", "sdds"]
+    probs = [Problem(labels[i % len(labels)], 17 + i % 23, 9 + i % 31, 5 + i % 40, seed=1000 + i) for i in range(300)]
+    want = []
+    for p in probs:
+        c = p.C.clone()
+        va, vb, vc = p.views(C=c)
+        M.gemm(_alpha(p.label), va, vb, SCALARS["cfg2_beta"], vc, cfg)
+        want.append(c)
+    calls = [(_alpha(p.label), *p.views()[:2], SCALARS["cfg2_beta"], p.views()[2]) for p in probs]
+    ks = _batch_with_profile(calls, cfg)
+    assert ks["dual_d"]["launches"] >= 2, ks
+    for p, w in zip(probs, want):
+        assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
