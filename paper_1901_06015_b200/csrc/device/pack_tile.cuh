@@ -1,0 +1,132 @@
+// One 32x32 source tile of a typecasting pack (Standard / 1e / 1r, left or
+// right panels, conjugation, alpha scaling) -- the body of pack.cu's kernels.  Bit-exact against the
+// reference pack (packing.cpp:114-230):
+//   v = widen(src) -> conj (src.conj xor requested) -> round to the target
+//   precision -> if scale != 1: complex<double> product, round again.
+// The tile moves through shared memory, read coalesced along the source's
+// unit-stride axis and written coalesced along the packed panels' contiguous
+// axis.
+#pragma once
+
+#include "common.cuh"
+
+namespace mdg {
+namespace packtile {
+
+constexpr int TILE = 32;
+using Tile = double2[TILE][TILE + 1];
+
+template <typename S, bool SRC_COMPLEX>
+__device__ __forceinline__ double2 load_src(const DView& v, int64_t i, int64_t j) {
+  const S* p = reinterpret_cast<const S*>(v.base) + (i * v.rs + j * v.cs) * (SRC_COMPLEX ? 2 : 1);
+  if constexpr (SRC_COMPLEX) {
+    return make_double2(static_cast<double>(p[0]), static_cast<double>(p[1]));
+  } else {
+    return make_double2(static_cast<double>(p[0]), 0.0);
+  }
+}
+
+__device__ __forceinline__ double2 process(double2 v, const PackDesc& d) {
+  if (d.do_conj) v.y = -v.y;
+  const bool sp = d.target_single;
+  double re = rnd(v.x, sp), im = rnd(v.y, sp);
+  if (!d.unit_scale) {
+    const double2 p = cmul(re, im, d.sre, d.sim);
+    re = rnd(p.x, sp);
+    im = rnd(p.y, sp);
+  }
+  return make_double2(re, im);
+}
+
+template <typename D>
+struct Pair;
+template <>
+struct Pair<float> {
+  using T = float2;
+  static __device__ __forceinline__ T make(double a, double b) {
+    return make_float2(static_cast<float>(a), static_cast<float>(b));
+  }
+};
+template <>
+struct Pair<double> {
+  using T = double2;
+  static __device__ __forceinline__ T make(double a, double b) { return make_double2(a, b); }
+};
+
+// Tile `bid` (source tiles column-major over ext_i x ext_j) by NT threads
+// (thread t of NT); sync() separates the staging from the stores.
+template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE, int NT, class Sync>
+__device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst, int64_t bid, Tile& tile, int t,
+                                          Sync sync) {
+  constexpr int ROWS = NT / 32;  // warps: tile rows per pass
+  const int64_t tiles_i = (d.ext_i + TILE - 1) / TILE;
+  const int64_t i0 = (bid % tiles_i) * TILE;
+  const int64_t j0 = (bid / tiles_i) * TILE;
+  const int lane = t & 31, row = t >> 5;
+
+  // Load: coalesce along the source's unit-stride axis.
+  const bool i_fast = d.src.rs <= d.src.cs;
+#pragma unroll
+  for (int r = 0; r < TILE / ROWS; ++r) {
+    const int ii = i_fast ? lane : row + ROWS * r;
+    const int jj = i_fast ? row + ROWS * r : lane;
+    const int64_t i = i0 + ii, j = j0 + jj;
+    double2 v = make_double2(0.0, 0.0);  // padded slots take literal zeros
+    if (i < d.src.m && j < d.src.n) v = process(load_src<S, SRC_COMPLEX>(d.src, i, j), d);
+    tile[jj][ii] = v;
+  }
+  sync();
+
+  // Store: coalesce along the packed buffer's contiguous axis.
+  const int64_t PD = d.pd, LP = d.lpad;
+#pragma unroll
+  for (int r = 0; r < TILE / ROWS; ++r) {
+    const int ii = SIDE == MDG_SIDE_LEFT ? lane : row + ROWS * r;
+    const int jj = SIDE == MDG_SIDE_LEFT ? row + ROWS * r : lane;
+    const int64_t i = i0 + ii, j = j0 + jj;
+    if (i >= d.ext_i || j >= d.ext_j) continue;
+    const double2 v = tile[jj][ii];
+    // offset of packed-logical (pr, pc) in block elements; power-of-two panel
+    // dims (every kernel tile) avoid the 64-bit division per element
+    const int sh = d.pd_shift;
+    auto off = [&](int64_t pr, int64_t pc) -> int64_t {
+      const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
+      if (sh >= 0) return ((x >> sh) * LP + y) * PD + (x & (PD - 1));
+      return (x / PD) * PD * LP + y * PD + x % PD;
+    };
+    if constexpr (FMT == MDG_FMT_STANDARD) {
+      if constexpr (SRC_COMPLEX) {
+        reinterpret_cast<typename Pair<D>::T*>(dst)[off(i, j)] = Pair<D>::make(v.x, v.y);
+      } else {
+        dst[off(i, j)] = static_cast<D>(v.x);
+      }
+    } else if constexpr (FMT == MDG_FMT_ONEE) {
+      using P = typename Pair<D>::T;
+      if constexpr (SIDE == MDG_SIDE_LEFT) {
+        // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, -im], [im, re]]
+        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
+        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j + 1)) = Pair<D>::make(-v.y, v.x);
+      } else {
+        // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, im], [-im, re]]
+        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
+        *reinterpret_cast<P*>(dst + off(2 * i + 1, 2 * j)) = Pair<D>::make(-v.y, v.x);
+      }
+    } else {  // 1r
+      if constexpr (SIDE == MDG_SIDE_LEFT) {
+        dst[off(i, 2 * j)] = static_cast<D>(v.x);
+        dst[off(i, 2 * j + 1)] = static_cast<D>(v.y);
+      } else {
+        dst[off(2 * i, j)] = static_cast<D>(v.x);
+        dst[off(2 * i + 1, j)] = static_cast<D>(v.y);
+      }
+    }
+  }
+}
+
+// Source tiles of a pack (the grid of pack.cu's kernels).
+__host__ __device__ inline int64_t pack_tiles(const PackDesc& d) {
+  return ((d.ext_i + TILE - 1) / TILE) * ((d.ext_j + TILE - 1) / TILE);
+}
+
+}  // namespace packtile
+}  // namespace mdg
