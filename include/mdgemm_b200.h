@@ -190,6 +190,15 @@ int mdg_gemm_batch(int32_t count, const mdg_gemm_call_t* calls, const mdg_config
 int mdg_gemm_batch_async(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg,
                          void* stream, uint64_t* flops_out);
 
+/* The launch schedule mdg_gemm_batch would use on the dual-pipe kernel, computed
+ * on the host without touching a device (tests / tooling): *npieces entries of
+ * five int32 {launch, call, tile begin, tile end, group} (group 1 = FP64 job,
+ * 2 = FP32 job, 0 = the call runs through mdg_execute in that launch slot),
+ * at most `capacity` written; call_tiles[i] = the tiles of call i (0 if not a
+ * dual job).  *npieces = 0 when the batch would not take the dual path. */
+int mdg_dual_schedule(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg, int32_t capacity,
+                      int32_t* pieces, int32_t* npieces, int32_t* call_tiles);
+
 /* Same with device pointers only, stream-ordered, no synchronisation. */
 int mdg_gemm_async(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b,
                    mdg_scalar_t beta, const mdg_view_t* c, const mdg_config_t* cfg,

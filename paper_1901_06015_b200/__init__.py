@@ -251,6 +251,8 @@ def _load() -> ctypes.CDLL:
         "mdg_gemm_async": (c_int, [S, V, V, S, V, C, c_void_p, POINTER(c_uint64)]),
         "mdg_gemm_batch": (c_int, [c_int32, POINTER(GemmCall), C, POINTER(c_uint64)]),
         "mdg_gemm_batch_async": (c_int, [c_int32, POINTER(GemmCall), C, c_void_p, POINTER(c_uint64)]),
+        "mdg_dual_schedule": (c_int, [c_int32, POINTER(GemmCall), C, c_int32, POINTER(c_int32), POINTER(c_int32),
+                                      POINTER(c_int32)]),
         "mdg_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64, c_int64]),
         "mdg_pack_operand": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
         "mdg_fill_uniform": (c_int, [V, c_uint64, c_void_p]),
@@ -273,6 +275,7 @@ EXPORTED_SYMBOLS = (
     "mdg_abi_version", "mdg_last_error", "mdg_config_defaults", "mdg_config_set", "mdg_config_load",
     "mdg_config_validate", "mdg_view_make", "mdg_classify_case", "mdg_flops_of_case", "mdg_apply_scalar_policy",
     "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_batch_async", "mdg_gemm_async",
+    "mdg_dual_schedule",
     "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
     "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
@@ -365,6 +368,26 @@ def gemm_batch(calls, cfg: Config | None = None, stream=None, sync: bool = True)
         _check(lib.mdg_gemm_batch_async(len(calls), arr, byref(cfg or Config.defaults()), _stream_ptr(stream),
                                         byref(flops)))
     return flops.value
+
+
+def dual_schedule(calls, cfg: Config | None = None):
+    """The dual-pipe launch schedule gemm_batch would use for `calls`, computed on the
+    host without a device: ([(launch, call, tile_begin, tile_end, group), ...], tiles per
+    call); group 1 = FP64 job, 2 = FP32 job, 0 = the call runs through execute().
+    Empty when the batch would not take the dual path."""
+    n = len(calls)
+    arr = (GemmCall * max(n, 1))(*[GemmCall(al, a, b, be, c) for al, a, b, be, c in calls])
+    cap = 4 * max(n, 1) + 64
+    while True:
+        pieces = (c_int32 * (5 * cap))()
+        tiles = (c_int32 * max(n, 1))()
+        count = c_int32(0)
+        _check(lib.mdg_dual_schedule(n, arr, byref(cfg or Config.defaults()), cap, pieces, byref(count), tiles))
+        if count.value <= cap:
+            break
+        cap = count.value
+    out = [tuple(pieces[5 * x:5 * x + 5]) for x in range(count.value)]
+    return out, list(tiles[:n])
 
 
 def gemm_async(alpha: Scalar, a: MatrixView, b: MatrixView, beta: Scalar, c: MatrixView,

@@ -298,6 +298,25 @@ int mdg_gemm_batch(int32_t count, const mdg_gemm_call_t* calls, const mdg_config
   });
 }
 
+int mdg_dual_schedule(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg, int32_t capacity,
+                      int32_t* pieces, int32_t* npieces, int32_t* call_tiles) {
+  return guarded([&] {
+    std::vector<int32_t> tiles;
+    const std::vector<DualPiece> out = dual_schedule_pieces(call_list(count, calls), config_from(cfg), &tiles);
+    *npieces = static_cast<int32_t>(out.size());
+    for (size_t x = 0; x < out.size() && static_cast<int32_t>(x) < capacity; ++x) {
+      int32_t* q = pieces + 5 * x;
+      q[0] = out[x].unit;
+      q[1] = out[x].call;
+      q[2] = out[x].t0;
+      q[3] = out[x].t1;
+      q[4] = out[x].group;
+    }
+    if (call_tiles)
+      for (int32_t i = 0; i < count; ++i) call_tiles[i] = tiles[static_cast<size_t>(i)];
+  });
+}
+
 int mdg_gemm_batch_async(int32_t count, const mdg_gemm_call_t* calls, const mdg_config_t* cfg, void* stream,
                          uint64_t* flops_out) {
   return guarded([&] {

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -72,6 +73,16 @@ void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* 
 // One dual launch over d's job lists (grid = SMs); flops per group for the
 // profiling hook.
 void dual_launch(const mdg::DualDesc& d, double flops_d, double flops_f, cudaStream_t st);
+
+// The dual-pipe batch schedule of gemm_batch (host only, no device work): one
+// entry per launch piece -- launch, call, tile range, group (1 FP64, 2 FP32;
+// 0 = the call runs through execute() in that slot).  Empty when the batch
+// would not take the dual path.  call_tiles: tiles of each dual call.
+struct DualPiece {
+  int32_t unit, call, t0, t1, group;
+};
+std::vector<DualPiece> dual_schedule_pieces(const std::vector<GemmCall>& calls, const Config& cfg,
+                                            std::vector<int32_t>* call_tiles);
 
 // The value the reference's FlopCounter reaches for this plan.
 uint64_t reference_flops(const ExecutionPlan& p);

@@ -1042,6 +1042,41 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
 
 }  // namespace
 
+std::vector<DualPiece> dual_schedule_pieces(const std::vector<GemmCall>& calls, const Config& cfg,
+                                            std::vector<int32_t>* call_tiles) {
+  std::vector<Call> cs(calls.size());
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const GemmCall& g = calls[i];
+    if (ranges_overlap(g.c, g.a) || ranges_overlap(g.c, g.b)) throw Error("gemm: C must not alias A or B");
+    cs[i].plan = plan(g.alpha, g.a, g.b, g.beta, g.c, cfg);
+    Call& c = cs[i];
+    const ExecutionPlan& p = c.plan;
+    c.active = p.m > 0 && p.n > 0;
+    const MatrixView* originals[3] = {&g.a, &g.b, &g.c};
+    const bool need[3] = {c.active && p.k > 0, c.active && p.k > 0, c.active};
+    for (int r = 0; r < 3; ++r) {
+      if (!need[r]) continue;
+      const auto [lo, hi] = byte_range(*originals[r]);
+      c.win[r] = Window{lo, hi};
+      c.host[r] = !c.win[r].empty();  // addresses only: no device is touched
+    }
+  }
+  DualPlan dp;
+  std::vector<DualPiece> out;
+  if (call_tiles) call_tiles->assign(calls.size(), 0);
+  if (!dual_schedule(cs, cfg, dp)) return out;
+  for (size_t i = 0; i < calls.size(); ++i)
+    if (call_tiles && dp.kind[i]) (*call_tiles)[i] = dp.prep[i].tiles;
+  for (size_t u = 0; u < dp.units.size(); ++u) {
+    const Unit& un = dp.units[u];
+    if (un.classic >= 0) out.push_back(DualPiece{static_cast<int32_t>(u), static_cast<int32_t>(un.classic), 0, 0, 0});
+    for (int grp = 0; grp < 2; ++grp)
+      for (const Piece& pc : grp == 0 ? un.d : un.f)
+        out.push_back(DualPiece{static_cast<int32_t>(u), static_cast<int32_t>(pc.call), pc.t0, pc.t1, grp + 1});
+  }
+  return out;
+}
+
 void staging_bytes(uint64_t* h2d, uint64_t* d2h) {
   if (h2d) *h2d = g_h2d_bytes.load(std::memory_order_relaxed);
   if (d2h) *d2h = g_d2h_bytes.load(std::memory_order_relaxed);
