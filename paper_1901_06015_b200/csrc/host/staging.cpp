@@ -372,6 +372,8 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
     if (npred[i] == 0) ready.push_back(i);
   std::sort(ready.begin(), ready.end(), by_priority);
   size_t done = 0;
+  size_t left_d = 0, left_f = 0;  // dual calls not finished yet, per kind
+  for (size_t i = 0; i < n; ++i) (kind[i] == 1 ? left_d : left_f) += kind[i] != 0;
   while (done < n) {
     Unit u;
     auto it = std::find_if(ready.begin(), ready.end(), [&](size_t i) { return kind[i] == 0; });
@@ -380,8 +382,15 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
     } else {
       double td = 0, tf = 0;
       for (size_t i : ready) (kind[i] == 1 ? td : tf) += rem_est(i);
-      const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? td / 2 : td);
-      const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (units.empty() ? tf / 2 : tf);
+      // Only one kind ready while the other kind still has work to come (all
+      // chains at the same phase, e.g. the first launch): take about half of
+      // the ready work, in whole calls, so the next launch pairs the rest with
+      // the successors of this half.  Otherwise pair min(td, tf) of each.
+      const bool one_sided = (td > 0) != (tf > 0);
+      const bool other_left = td > 0 ? left_f > 0 : left_d > 0;
+      const bool halve = one_sided && other_left;
+      const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? td / 2 : td);
+      const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? tf / 2 : tf);
       // in priority order, whole remaining ranges that keep each side within
       // 5 % of its target; then a side that fell short takes part of its next
       // call's tiles
@@ -415,7 +424,8 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
         const int32_t left = prep[i].tiles - next_tile[i];
         const double per_tile = est[i] / prep[i].tiles;
         const int32_t want = static_cast<int32_t>(std::ceil((target - acc) / per_tile));
-        take(i, std::max<int32_t>(1, std::min(left, want)));
+        // (halving keeps whole calls: their successors are what the next launch pairs with)
+        take(i, halve ? left : std::max<int32_t>(1, std::min(left, want)));
         used[x] = 1;
       }
     }
@@ -433,7 +443,11 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
       first_unit[static_cast<size_t>(u.classic)] = uid;
       finished.push_back(static_cast<size_t>(u.classic));
     }
-    for (size_t i : finished) ready.erase(std::find(ready.begin(), ready.end(), i));
+    for (size_t i : finished) {
+      ready.erase(std::find(ready.begin(), ready.end(), i));
+      if (kind[i] == 1) --left_d;
+      if (kind[i] == 2) --left_f;
+    }
     done += finished.size();
     std::vector<size_t> newly;
     for (size_t i : finished)
