@@ -320,10 +320,8 @@ int main(int argc, char** argv) {
          " F = FFMA2 (NF*16)x128 tiles\n", sms, lpad);
   // name, ND, DWM, NF, DSTAGES, FSTAGES, RD, RF, RP ; waves chosen so D and F take similar time
   // (F flops per tile-wave = BM_F/BM_D x D's, at ~2x the rate)
-  config<4, 64, 8, 4, 6, 168, 128, 56>("d4(64x32) f8 smr168/128", sms, da, db, fa, fb, sink, t_end, nk, 4, 4);
   config<8, 64, 4, 3, 6, 168, 0, 40>("d8(64x32) f4 smr168/-/40", sms, da, db, fa, fb, sink, t_end, nk, 2, 4);
-  config<8, 64, 4, 3, 6, 168, 0, 40>("d8(64x32) f4 smr168 F2x", sms, da, db, fa, fb, sink, t_end, nk, 2, 8);
-  config<8, 64, 4, 3, 4, 168, 0, 40>("d8(64x32) f4 fst4", sms, da, db, fa, fb, sink, t_end, nk, 2, 4);
-  config<8, 32, 8, 4, 6, 104, 120, 32>("d8(32x32) f8 smr104/120", sms, da, db, fa, fb, sink, t_end, nk, 4, 4);
+  config<12, 32, 4, 3, 6, 104, 144, 24>("d12(32x32) f4 smr104/144/24", sms, da, db, fa, fb, sink, t_end, nk, 3, 4);
+  config<12, 32, 4, 3, 6, 104, 144, 24>("d12(32x32) f4 F2x", sms, da, db, fa, fb, sink, t_end, nk, 3, 8);
   return 0;
 }
