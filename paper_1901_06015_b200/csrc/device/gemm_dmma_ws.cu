@@ -417,6 +417,258 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
   }
 }
 
+// ------------------------------------------------------------------------
+// Variant with epilogue warps (real single-precision C, swizzled C tile):
+// the MMA warps only round their accumulators to C's precision and dump them
+// into a stage buffer laid out like the C tile, then start the next tile's
+// mainloop; six epilogue warps combine stage and C tile (accumulate_element,
+// 16-byte vectors, conflict-free) while the MMA warps compute.  For short k
+// (cfg5: k = 64 is 4 k-blocks per tile) the combine pass otherwise runs
+// between two mainloops with the DMMA pipe idle.
+//   warps 0-7   MMA (setmaxnreg 168)
+//   warp  8     producer lane;  warp 9: C mover lane
+//   warps 10-15 epilogue (warpgroups 2-3: setmaxnreg 88)
+constexpr int WE_THREADS = 512;
+constexpr int WE_EPI_WARP0 = 10, WE_EPI_WARPS = 6;
+constexpr int WE_STAGES = 3;
+constexpr size_t WE_RING = size_t(WE_STAGES) * (WS_STAGE_A + WS_STAGE_B) * sizeof(double);  // 96 KB
+constexpr size_t WE_CTILE = size_t(WS_BM) * WS_BN * sizeof(float);                         // 64 KB
+constexpr size_t WE_SMEM = WE_RING + 2 * WE_CTILE + (2 * WE_STAGES + 4) * sizeof(uint64_t);
+
+__global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const __grid_constant__ GemmDesc d) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double* sA = reinterpret_cast<double*>(smem);
+  double* sB = sA + WE_STAGES * WS_STAGE_A;
+  unsigned char* ctile = smem + WE_RING;              // C (TMA, swizzled boxes)
+  unsigned char* stage = ctile + WE_CTILE;            // rounded results, same layout
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + WE_CTILE);
+  uint64_t* empty = full + WE_STAGES;
+  uint64_t* c_full = empty + WE_STAGES;  // mover -> epilogue: this tile's C is in ctile
+  uint64_t* staged = c_full + 1;         // MMA warps -> epilogue: results in stage (8 arrivals)
+  uint64_t* stage_free = staged + 1;     // epilogue -> MMA warps: stage read (6 arrivals)
+  uint64_t* res_full = stage_free + 1;   // epilogue -> mover: ctile combined (6 arrivals)
+
+  const int tiles_m = static_cast<int>((d.me + WS_BM - 1) / WS_BM);
+  const int tiles_n = static_cast<int>((d.ne + WS_BN - 1) / WS_BN);
+  const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
+  const int64_t lpad = d.a.lpad;
+  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (smem_u32(ctile) & 1023) __trap();  // the 128-byte swizzle needs 1 KB-aligned boxes
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < WE_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], WS_MMA_WARPS);
+    }
+    mbar_init(c_full, 1);
+    mbar_init(staged, WS_MMA_WARPS);
+    mbar_init(stage_free, WE_EPI_WARPS);
+    mbar_init(res_full, WE_EPI_WARPS);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp >= WS_MMA_WARPS) {  // ---------------------------- producer, mover, epilogue
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n");
+    const DEpilogue& e = d.epi;
+    const bool reads_c = !e.beta.is_zero;
+    constexpr int RB = 32, NRB = WS_BM / RB;  // 128-byte box lines of floats
+    auto coords = [&](const Seg& sg, int& x0, int& y0) {
+      int tm, tn;
+      tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+      x0 = tm * WS_BM;
+      y0 = tn * WS_BN;
+    };
+    if (warp == WS_PROD_WARP) {
+      if (lane != 0) return;
+      int it = 0;
+      for (int si = 0; si < sc.nseg; ++si) {
+        const Seg sg = ws_seg(sc, si);
+        int tm, tn;
+        tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * WS_BM * lpad;
+        const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * WS_BN * lpad;
+        for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+          const int s = it % WE_STAGES;
+          if (it >= WE_STAGES) mbar_wait(&empty[s], ((it / WE_STAGES) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], (WS_STAGE_A + WS_STAGE_B) * sizeof(double));
+          bulk_g2s(sA + s * WS_STAGE_A, Ag + static_cast<int64_t>(kb) * WS_STAGE_A, WS_STAGE_A * sizeof(double),
+                   &full[s]);
+          bulk_g2s(sB + s * WS_STAGE_B, Bg + static_cast<int64_t>(kb) * WS_STAGE_B, WS_STAGE_B * sizeof(double),
+                   &full[s]);
+        }
+      }
+      return;
+    }
+    if (warp == WS_CMOV_WARP) {
+      if (lane != 0) return;
+      auto boxes = [&](int x0, int y0, bool load) {
+        for (int b = 0; b < WS_BN / C_BOX_COLS; ++b)
+          for (int rb = 0; rb < NRB; ++rb) {
+            unsigned char* box = ctile + static_cast<size_t>(b * NRB + rb) * 2048;
+            if (load)
+              tensor_load_2d(box, &e.cmap_sw, x0 + rb * RB, y0 + b * C_BOX_COLS, c_full);
+            else
+              tensor_store_2d(&e.cmap_sw, x0 + rb * RB, y0 + b * C_BOX_COLS, box);
+          }
+      };
+      int epis = 0, pending = -1;
+      for (int si = 0; si < sc.nseg; ++si) {
+        const Seg sg = ws_seg(sc, si);
+        if (sg.kind == SEG_START) continue;
+        if (pending >= 0) {  // store the previous tile, then reuse the buffer for this one
+          mbar_wait(res_full, epis & 1);
+          int x0, y0;
+          coords(ws_seg(sc, pending), x0, y0);
+          boxes(x0, y0, false);
+          bulk_commit();
+          bulk_wait_read();
+          ++epis;
+        }
+        fence_proxy_async();
+        if (reads_c) {
+          int x0, y0;
+          coords(sg, x0, y0);
+          mbar_arrive_expect_tx(c_full, static_cast<uint32_t>(WE_CTILE));
+          boxes(x0, y0, true);
+        } else {
+          mbar_arrive(c_full);
+        }
+        pending = si;
+      }
+      if (pending >= 0) {
+        mbar_wait(res_full, epis & 1);
+        int x0, y0;
+        coords(ws_seg(sc, pending), x0, y0);
+        boxes(x0, y0, false);
+        bulk_commit();
+        bulk_wait_read();
+      }
+      return;
+    }
+    // epilogue warps: stage (+) C, in place in ctile, 16-byte vectors
+    if (warp < WE_EPI_WARP0) return;
+    const int et = threadIdx.x - WE_EPI_WARP0 * 32;
+    const float rb = static_cast<float>(e.beta.re);
+    const int mode = e.beta.is_zero ? 0 : (e.beta.is_one ? 1 : 2);
+    int epis = 0;
+    for (int si = 0; si < sc.nseg; ++si) {
+      if (ws_seg(sc, si).kind == SEG_START) continue;
+      mbar_wait(staged, epis & 1);
+      mbar_wait(c_full, epis & 1);
+      const float4* sv = reinterpret_cast<const float4*>(stage);
+      float4* cv = reinterpret_cast<float4*>(ctile);
+      constexpr int NV = static_cast<int>(WE_CTILE / 16);
+      for (int v = et; v < NV; v += WE_EPI_WARPS * 32) {
+        const float4 t = sv[v];
+        float4 c = cv[v];
+        if (mode == 0) {
+          c = t;
+        } else if (mode == 1) {
+          c.x = __fadd_rn(c.x, t.x);
+          c.y = __fadd_rn(c.y, t.y);
+          c.z = __fadd_rn(c.z, t.z);
+          c.w = __fadd_rn(c.w, t.w);
+        } else {
+          c.x = __fadd_rn(__fmul_rn(rb, c.x), t.x);
+          c.y = __fadd_rn(__fmul_rn(rb, c.y), t.y);
+          c.z = __fadd_rn(__fmul_rn(rb, c.z), t.z);
+          c.w = __fadd_rn(__fmul_rn(rb, c.w), t.w);
+        }
+        cv[v] = c;
+      }
+      fence_proxy_async();  // generic writes of ctile before the mover's TMA store reads them
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(stage_free);
+        mbar_arrive(res_full);
+      }
+      ++epis;
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- MMA warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+  const int tid = threadIdx.x;
+  const int wm = warp % WS_WM, wn = warp / WS_WM;
+  const int g = lane >> 2, tig = lane & 3;
+  const uint32_t full_u = smem_u32(full), empty_u = smem_u32(empty);
+  const double* a_base = sA + wm * 64 + g + tig * WS_BM;
+  const double* b_base = sB + wn * 32 + g + tig * WS_BN;
+  int it = 0, epis = 0;
+  for (int si = 0; si < sc.nseg; ++si) {
+    const Seg sg = ws_seg(sc, si);
+    double acc[WS_MT][WS_NT][2];
+    if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      if (tid == 0) flag_acquire_wait(d.sk_flags + blockIdx.x - 1);
+      named_sync(1, WS_MMA_THREADS);
+      const double* slot =
+          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x - 1) * (WS_BM * WS_BN);
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            acc[i][j][h] = __ldcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid);
+    } else {
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
+      const int s = it % WE_STAGES;
+      mbar_wait_u32(full_u + 8 * s, (it / WE_STAGES) & 1);
+      const double* a = a_base + s * WS_STAGE_A;
+      const double* b = b_base + s * WS_STAGE_B;
+#pragma unroll
+      for (int kk = 0; kk < WS_BK; kk += 4) {
+        double af[WS_MT], bf[WS_NT];
+#pragma unroll
+        for (int i = 0; i < WS_MT; ++i) af[i] = a[kk * WS_BM + i * 8];
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j) bf[j] = b[kk * WS_BN + j * 8];
+#pragma unroll
+        for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+          for (int j = 0; j < WS_NT; ++j) dmma884_ws(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
+    }
+    if (sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
+      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x) * (WS_BM * WS_BN);
+#pragma unroll
+      for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+        for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
+      __threadfence();
+      named_sync(1, WS_MMA_THREADS);
+      if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
+      continue;
+    }
+    // round to C's precision (accumulate_element's tc) into the stage buffer
+    if (epis > 0) mbar_wait(stage_free, (epis - 1) & 1);
+#pragma unroll
+    for (int i = 0; i < WS_MT; ++i)
+#pragma unroll
+      for (int j = 0; j < WS_NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm * 64 + i * 8 + g, c = wn * 32 + j * 8 + 2 * tig + h;
+          *reinterpret_cast<float*>(stage + ws_swz_off<4>(r, c)) = static_cast<float>(acc[i][j][h]);
+        }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(staged);
+    ++epis;
+  }
+}
+
 }  // namespace
 
 size_t dmma_ws_smem(int cdt) {
@@ -428,6 +680,18 @@ size_t dmma_ws_smem(int cdt) {
 cudaError_t launch_gemm_dmma_ws(const GemmDesc& d, int grid, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
+  // real single-precision C in swizzled boxes: the epilogue-warp variant
+  static const bool epi_warps = [] {
+    const char* f = std::getenv("MDGEMM_WS_EPI_WARPS");  // tuning: 0 = always the plain WS kernel
+    return f ? std::atoi(f) != 0 : true;
+  }();
+  if (epi_warps && d.epi.out.dtype == MDG_DT_S && d.epi.sw_ok && d.epi.pair == MDG_PAIR_NONE) {
+    e = cudaFuncSetAttribute(gemm_dmma_ws_epi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(WE_SMEM));
+    if (e != cudaSuccess) return e;
+    gemm_dmma_ws_epi_kernel<<<static_cast<unsigned>(grid), WE_THREADS, WE_SMEM, s>>>(d);
+    return cudaGetLastError();
+  }
   MDG_DISPATCH_CDT(d.epi.out.dtype, CDT, {
     auto kern = gemm_dmma_ws_kernel<CDT>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(WsCfg<CDT>::SMEM));
