@@ -142,12 +142,15 @@ size_t unique_host_bytes(std::vector<Window> w) {
 size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  size_t free_b = 0, total_b = 0;
-  cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   static std::mutex mu;
   static std::vector<size_t> reserved;
   std::lock_guard<std::mutex> lock(mu);
   if (reserved.size() <= static_cast<size_t>(dev)) reserved.resize(dev + 1, 0);
+  // Device operands only and the pool already holds the arenas: nothing to
+  // decide (and no cudaMemGetInfo, which stalled lone-call enqueues)
+  if (host_bytes == 0 && arena_bytes * static_cast<size_t>(nstreams) <= reserved[dev]) return 0;
+  size_t free_b = 0, total_b = 0;
+  cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
   // residents may use what the pool already holds plus half of what is free
   const size_t arenas = arena_bytes * static_cast<size_t>(nstreams);
   const size_t room = reserved[dev] + free_b / 2;
