@@ -160,6 +160,12 @@ constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128,
 
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);
+// Both packs of a call in one launch; valid when pack_pair_ok (same source
+// type, target precision and format), else it falls back to two launches.
+cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s);
+inline bool pack_pair_ok(const PackDesc& a, const PackDesc& b) {
+  return a.src.dtype == b.src.dtype && a.target_single == b.target_single && a.format == b.format;
+}
 cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s);
 cudaError_t launch_fill_uniform(const DView& v, uint64_t state, cudaStream_t s);
 cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, cudaStream_t s);

@@ -23,6 +23,61 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_kernel(PackDesc d, D* __res
                                                                    [] { __syncthreads(); });
 }
 
+// Both operands of a call in one launch when they share source type, target
+// precision and format (the side is decided per CTA): one launch instead of
+// two, and the two packs' tiles share the waves.
+template <typename S, bool SRC_COMPLEX, typename D, int FMT>
+__global__ void __launch_bounds__(PACK_THREADS)
+    pack_pair_kernel(const __grid_constant__ PackDesc d0, D* __restrict__ dst0, const __grid_constant__ PackDesc d1,
+                     D* __restrict__ dst1, int64_t tiles0) {
+  __shared__ packtile::Tile tile;
+  const bool first = static_cast<int64_t>(blockIdx.x) < tiles0;
+  const PackDesc& d = first ? d0 : d1;
+  D* dst = first ? dst0 : dst1;
+  const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
+  auto sync = [] { __syncthreads(); };
+  if (d.side == MDG_SIDE_LEFT)
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+  else
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+}
+
+template <typename S, bool SC, typename D, int FMT>
+cudaError_t go_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
+  const int64_t ta = packtile::pack_tiles(a), tb = packtile::pack_tiles(b);
+  if (ta + tb == 0) return cudaSuccess;
+  if (ta + tb > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  pack_pair_kernel<S, SC, D, FMT><<<static_cast<unsigned>(ta + tb), PACK_THREADS, 0, s>>>(
+      a, static_cast<D*>(da), b, static_cast<D*>(db), ta);
+  return cudaGetLastError();
+}
+
+template <typename S, bool SC, typename D>
+cudaError_t go_pair_format(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
+  if constexpr (SC) {
+    if (a.format == MDG_FMT_ONEE) return go_pair<S, SC, D, MDG_FMT_ONEE>(a, da, b, db, s);
+    if (a.format == MDG_FMT_ONER) return go_pair<S, SC, D, MDG_FMT_ONER>(a, da, b, db, s);
+  }
+  if (a.format != MDG_FMT_STANDARD) return cudaErrorInvalidValue;
+  return go_pair<S, SC, D, MDG_FMT_STANDARD>(a, da, b, db, s);
+}
+
+template <typename S, bool SC>
+cudaError_t go_pair_target(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
+  return a.target_single ? go_pair_format<S, SC, float>(a, da, b, db, s)
+                         : go_pair_format<S, SC, double>(a, da, b, db, s);
+}
+
+cudaError_t pad(const PackDesc& d, void* dst, cudaStream_t s) {
+  if (d.lpad <= d.len || d.panels == 0) return cudaSuccess;
+  // Zero the inner-dimension padding rows [len, lpad) of every panel.
+  const size_t esz = (d.target_single ? 4 : 8) * (d.out_complex ? 2 : 1);
+  const size_t pitch = static_cast<size_t>(d.pd * d.lpad) * esz;
+  const size_t width = static_cast<size_t>(d.pd * (d.lpad - d.len)) * esz;
+  char* first = static_cast<char*>(dst) + static_cast<size_t>(d.pd * d.len) * esz;
+  return cudaMemset2DAsync(first, pitch, 0, width, static_cast<size_t>(d.panels), s);
+}
+
 template <typename S, bool SC, typename D, int FMT>
 cudaError_t go_side(const PackDesc& d, void* dst, cudaStream_t s) {
   const int64_t tiles = packtile::pack_tiles(d);
@@ -62,13 +117,26 @@ cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s) {
     case MDG_DT_Z: e = go_target<double, true>(d, dst, s); break;
     default: return cudaErrorInvalidValue;
   }
-  if (e != cudaSuccess || d.lpad <= d.len || d.panels == 0) return e;
-  // Zero the inner-dimension padding rows [len, lpad) of every panel.
-  const size_t esz = (d.target_single ? 4 : 8) * (d.out_complex ? 2 : 1);
-  const size_t pitch = static_cast<size_t>(d.pd * d.lpad) * esz;
-  const size_t width = static_cast<size_t>(d.pd * (d.lpad - d.len)) * esz;
-  char* first = static_cast<char*>(dst) + static_cast<size_t>(d.pd * d.len) * esz;
-  return cudaMemset2DAsync(first, pitch, 0, width, static_cast<size_t>(d.panels), s);
+  if (e != cudaSuccess) return e;
+  return pad(d, dst, s);
+}
+
+cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
+  if (a.src.dtype != b.src.dtype || a.target_single != b.target_single || a.format != b.format) {
+    const cudaError_t e = launch_pack(a, da, s);
+    return e != cudaSuccess ? e : launch_pack(b, db, s);
+  }
+  cudaError_t e = cudaSuccess;
+  switch (a.src.dtype) {
+    case MDG_DT_S: e = go_pair_target<float, false>(a, da, b, db, s); break;
+    case MDG_DT_D: e = go_pair_target<double, false>(a, da, b, db, s); break;
+    case MDG_DT_C: e = go_pair_target<float, true>(a, da, b, db, s); break;
+    case MDG_DT_Z: e = go_pair_target<double, true>(a, da, b, db, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e == cudaSuccess) e = pad(a, da, s);
+  if (e == cudaSuccess) e = pad(b, db, s);
+  return e;
 }
 
 }  // namespace mdg

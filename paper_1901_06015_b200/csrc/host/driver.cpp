@@ -447,13 +447,18 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   char* wsa = static_cast<char*>(ws);
   cudaError_t err = flag_bytes > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
   cuda_check(err, "stream-K flags");
-  {
-    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes));
-    err = mdg::launch_pack(pa.desc, wsa, st);
-  }
-  if (err == cudaSuccess) {
-    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, pb.bytes));
-    err = mdg::launch_pack(pb.desc, wsa + off_b, st);
+  if (mdg::pack_pair_ok(pa.desc, pb.desc)) {  // both operands in one launch
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes) + pack_traffic(p.b, pb.bytes));
+    err = mdg::launch_pack_pair(pa.desc, wsa, pb.desc, wsa + off_b, st);
+  } else {
+    {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes));
+      err = mdg::launch_pack(pa.desc, wsa, st);
+    }
+    if (err == cudaSuccess) {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, pb.bytes));
+      err = mdg::launch_pack(pb.desc, wsa + off_b, st);
+    }
   }
 
   mdg::GemmDesc g{};
@@ -593,13 +598,18 @@ DualPrep dual_prepare(const ExecutionPlan& p) {
 void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job) {
   const DualPrep d = dual_prepare(p);
   char* w = static_cast<char*>(ws);
-  {
-    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a));
-    cuda_check(mdg::launch_pack(d.pa, w, st), "pack kernel");
-  }
-  {
-    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, d.bytes_b));
-    cuda_check(mdg::launch_pack(d.pb, w + d.off_b, st), "pack kernel");
+  if (mdg::pack_pair_ok(d.pa, d.pb)) {
+    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a) + pack_traffic(p.b, d.bytes_b));
+    cuda_check(mdg::launch_pack_pair(d.pa, w, d.pb, w + d.off_b, st), "pack kernel");
+  } else {
+    {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a));
+      cuda_check(mdg::launch_pack(d.pa, w, st), "pack kernel");
+    }
+    {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, d.bytes_b));
+      cuda_check(mdg::launch_pack(d.pb, w + d.off_b, st), "pack kernel");
+    }
   }
   const int64_t bm = d.single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
   const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
