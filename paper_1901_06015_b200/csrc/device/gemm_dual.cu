@@ -365,13 +365,14 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     const double* a_base = dA + wm * 64 + g + tig * DD_BM;
     const double* b_base = dB + wn * 32 + g + tig * DD_BN;
     const uint32_t full_u = smem_u32(dfull), empty_u = smem_u32(dempty);
-    int it = 0;
+    // ring position as (stage, phase) counters: no division by the 3-stage
+    // ring in the k loop of the group that bounds the pairing
+    int st = 0;
+    uint32_t ph = 0;
     for (;;) {
-      {  // the producer names the next tile in its first stage's slot
-        const int s0 = it % DD_STAGES;
-        mbar_wait_u32(full_u + 8 * s0, (it / DD_STAGES) & 1);
-      }
-      int v = *reinterpret_cast<volatile int*>(&dslot[it % DD_STAGES]);
+      // the producer names the next tile in its first stage's slot
+      mbar_wait_u32(full_u + 8 * st, ph);
+      int v = *reinterpret_cast<volatile int*>(&dslot[st]);
       if (v < 0) break;
       // only v stays live through the mainloop (the group runs at its register
       // cap); the job and tile coordinates are derived again for the epilogue
@@ -381,9 +382,9 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % DD_STAGES;
-        if (kb > 0) mbar_wait_u32(full_u + 8 * s, (it / DD_STAGES) & 1);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = st;
+        if (kb > 0) mbar_wait_u32(full_u + 8 * s, ph);
         const double* a = a_base + s * DD_SA;
         const double* b = b_base + s * DD_SB;
 #pragma unroll
@@ -401,6 +402,10 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         fence_proxy_async();  // generic reads of the stage before its TMA refill
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
+        if (++st == DD_STAGES) {
+          st = 0;
+          ph ^= 1;
+        }
       }
       asm volatile("" : "+r"(v));
       const int jx = job_of(d.d, d.nd, v);
