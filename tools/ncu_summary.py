@@ -19,12 +19,16 @@ ALGO = {
     "pack": 4096 * 4096 * 16 + 8192 * 8192 * 8,
     # dddd 4096 on the warp-specialised kernel: A + B packed f64, C read + written
     "dmma_ws": 4 * 4096 * 4096 * 8,
+    # cfg5 k=64 (sddd 32768^2 x 64) on the epilogue-warp WS kernel: A + B packed f64, C f32 read + written
+    "dmma_ws_epi": 2 * 32768 * 64 * 8 + 2 * 32768 * 32768 * 4,
 }
-FLOPS = {"dmma": 2.0 * 8192 * 4096 * 8192, "ffma": 2.0 * 8192 * 4096 * 8192, "dmma_ws": 2.0 * 4096 ** 3}
+FLOPS = {"dmma": 2.0 * 8192 * 4096 * 8192, "ffma": 2.0 * 8192 * 4096 * 8192, "dmma_ws": 2.0 * 4096 ** 3,
+         "dmma_ws_epi": 2.0 * 32768 * 32768 * 64}
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA subpipe % active"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe % active"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots active %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
@@ -50,12 +54,14 @@ def main():
     os.makedirs(dst, exist_ok=True)
     lines = ["# ncu --set full captures, round 1 (tools/profile_r01.sh, one launch each, --clock-control none)", "",
              "Launches: DMMA = `zzzd` 4096 (1m: me=8192, ne=4096, ke=8192), FFMA = `cccs` 4096 (same real dims), "
-             "pack = the 1e pack of `zzzd`'s A, dmma_ws = the warp-specialised DMMA kernel on a lone `dddd` 4096 call.  Per-launch times are cold-cache and serialised (ncu replays), so "
+             "pack = the 1e pack of `zzzd`'s A, dmma_ws = the warp-specialised DMMA kernel on a lone `dddd` 4096 call, "
+             "dmma_ws_epi = its epilogue-warp variant on cfg5 k=64 (`sddd` 32768^2 x 64), dual = one gemm_dual launch of "
+             "the batched 3584/4096 sweep slice (tools/profile_dual.sh).  Per-launch times are cold-cache and serialised (ncu replays), so "
              "compare shares, not absolutes, with bench.py.", ""]
     traffic = {"what": "dram__bytes_read.sum + dram__bytes_write.sum of one captured launch (ncu --set full): "
                        "dmma = zzzd 4096, ffma = cccs 4096, pack = zzzd's 1e pack of A; algorithmic bytes alongside",
                "algorithmic_bytes_per_launch": {}}
-    for k in ("dmma", "ffma", "pack", "dmma_ws"):
+    for k in ("dmma", "ffma", "pack", "dmma_ws", "dmma_ws_epi", "dual"):
         p = os.path.join(src, f"ncu_{k}_raw.csv")
         if not os.path.exists(p):
             continue
@@ -72,6 +78,11 @@ def main():
         wr = float(m["dram__bytes_write.sum"][0]) * SCALE.get(m["dram__bytes_write.sum"][1], 1)
         dur = float(m["gpu__time_duration.sum"][0]) * SCALE.get(m["gpu__time_duration.sum"][1], 1)
         traffic[k] = rd + wr
+        if k == "dual":  # both pipes: fp64 tensor ops counted by ncu, FP32 via the FMA pipe share
+            f64 = float(m["sm__ops_path_tensor_src_fp64.sum"][0])
+            lines.append(f"| FP64 tensor ops in the launch | {f64:.4g} = {f64 / dur / 1e12:.2f} TFLOP/s of DMMA work |")
+            lines.append("")
+            continue
         traffic["algorithmic_bytes_per_launch"][k] = ALGO[k]
         lines.append(f"| DRAM bytes / algorithmic bytes | {(rd + wr) / ALGO[k]:.2f} |")
         if k in FLOPS:

@@ -26,3 +26,13 @@ ncu --set full --clock-control none --import-source on -k regex:gemm_dmma_ws -s 
 echo dmma_ws_rc=$?
 ncu -i $O/prof_dmma_ws.ncu-rep --page raw --csv > $O/ncu_dmma_ws_raw.csv 2>/dev/null
 ncu -i $O/prof_dmma_ws.ncu-rep --page details --csv > $O/ncu_dmma_ws_details.csv 2>/dev/null
+# the epilogue-warp variant of the WS DMMA kernel (real single-precision C): cfg5 k=64
+C3="python bench.py --workload cfg5-k64 --steps 1 --warmup 1 --no-e2e --no-cpu --no-serial"
+$C3 > $O/plain_ws_epi.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:gemm_dmma_ws_epi -s 1 -c 1 -o $O/prof_dmma_ws_epi -f $C3 > $O/ncu_dmma_ws_epi.log 2>&1
+echo dmma_ws_epi_rc=$?
+ncu -i $O/prof_dmma_ws_epi.ncu-rep --page raw --csv > $O/ncu_dmma_ws_epi_raw.csv 2>/dev/null
+ncu -i $O/prof_dmma_ws_epi.ncu-rep --page details --csv > $O/ncu_dmma_ws_epi_details.csv 2>/dev/null
+# the dual-pipe kernel (batched sweep slice)
+bash tools/profile_dual.sh
+cp gpurun_out/profd/ncu_dual_raw.csv gpurun_out/profd/ncu_dual_details.csv gpurun_out/profd/launches.csv $O/ 2>/dev/null
