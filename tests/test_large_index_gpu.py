@@ -1,0 +1,42 @@
+"""Maximum sizes: views with more than 2**31 elements (and 2**32 bytes).
+
+The reference indexes with 64-bit integers throughout (`MatrixView` strides
+and offsets are int64_t, `include/mdgemm/types.hpp`); these cases check that
+no 32-bit product survives in the B200 path -- C tiles far past element 2**31
+(real and 1m complex images, both warp-specialised kernels), and an inner
+dimension long enough that the packed panels pass 2**31 elements.  Checked
+like the BASELINE-scale tests: sampled rows/columns (edges included) against
+the oracle with the full inner dimension."""
+import pytest
+
+import paper_1901_06015_b200 as M
+from tests.test_baseline_scale_gpu import run_config
+
+pytestmark = pytest.mark.gpu
+
+
+def _free():
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("label,m,n,k", [
+    ("ssss", 49152, 49152, 32),   # C: 2.4e9 floats (9.7 GB), FFMA WS kernel
+    ("sddd", 49152, 49152, 32),   # C: 2.4e9 floats, DMMA WS kernel
+    ("zzzd", 34816, 34816, 32),   # C: 1.2e9 complex = 2.4e9 doubles in the 1m real image
+])
+def test_c_past_2_31_elements(label, m, n, k):
+    assert m * n * (2 if label[0] in "cz" else 1) > 2**31
+    one, beta = M.Scalar.real_value(1.0), M.Scalar.real_value(0.5)
+    run_config(label, m, n, k, one, beta, "fast", seed=7, nsamp=10)
+    _free()
+
+
+def test_inner_dimension_past_2_31_packed_elements():
+    # A is 192 x 12e6 floats: the left pack's panel offsets pass 2**31 elements
+    m = n = 192
+    k = 12_000_000
+    assert m * k > 2**31
+    run_config("ssss", m, n, k, M.Scalar.real_value(1.0), M.Scalar.real_value(0.0), "fast", seed=8, nsamp=6)
+    _free()
