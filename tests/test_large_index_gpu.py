@@ -40,3 +40,35 @@ def test_inner_dimension_past_2_31_packed_elements():
     assert m * k > 2**31
     run_config("ssss", m, n, k, M.Scalar.real_value(1.0), M.Scalar.real_value(0.0), "fast", seed=8, nsamp=6)
     _free()
+
+
+def test_dual_batch_past_2_31_elements(monkeypatch):
+    """A mixed-precision batch on the dual-pipe kernel whose FP64 and FP32 calls each
+    have a C past 2**31 elements: bitwise equal to calling gemm() on each."""
+    import torch
+    from tests.test_baseline_scale_gpu import DevMat
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    cfg = M.Config.defaults()
+    m = n = 49152
+    k = 32
+    one, beta = M.Scalar.real_value(1.0), M.Scalar.real_value(0.5)
+    mats = {}
+    for label in ("sddd", "ssss"):
+        dc, da, db = (M.dtype_from_letter(ch) for ch in label[:3])
+        root = M.Rng(9).split(label)
+        mats[label] = (DevMat(da, m, k, root.split("a").state), DevMat(db, k, n, root.split("b").state),
+                       DevMat(dc, m, n, root.split("c").state), M.SINGLE if label[3] == "s" else M.DOUBLE)
+    want = {}
+    for label, (A, B, C, comp) in mats.items():
+        c = C.copy()
+        M.gemm(one, A.view(), B.view(), beta, c.view(comp), cfg)
+        want[label] = c
+    M.profile_begin()
+    M.gemm_batch([(one, A.view(), B.view(), beta, C.view(comp)) for A, B, C, comp in mats.values()], cfg)
+    ks = M.profile_end()
+    torch.cuda.synchronize()
+    assert ks["dual_d"]["launches"] > 0 and ks["dual_f"]["work"] > 0, ks  # one launch, both groups
+    for label, (A, B, C, comp) in mats.items():
+        assert torch.equal(C.t, want[label].t), label
+    del mats, want
+    _free()
