@@ -33,6 +33,13 @@ def test_c_past_2_31_elements(label, m, n, k):
     _free()
 
 
+def test_exact_c_past_2_31_elements():
+    # the EXACT replay kernel (gemm_exact.cu): bitwise the reference on sampled blocks
+    one, beta = M.Scalar.real_value(1.0), M.Scalar.complex_value(0.5, 0.25)
+    run_config("sdds", 49152, 49152, 8, one, beta, "exact", seed=5, nsamp=8, exact_bitwise=True)
+    _free()
+
+
 def test_inner_dimension_past_2_31_packed_elements():
     # A is 192 x 12e6 floats: the left pack's panel offsets pass 2**31 elements
     m = n = 192
