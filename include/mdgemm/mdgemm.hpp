@@ -196,6 +196,12 @@ struct Config {
   Preference preference = Preference::Column;
   CTempMode ctemp = CTempMode::Auto;
   Numerics numerics = Numerics::Fast;
+  // B200 extension (gpu.splitk = auto | off): FAST calls whose tile grid
+  // fills less than half of the GPU may split the inner dimension over
+  // several CTAs (deterministic, but a different summation order than the
+  // unsplit grid); off keeps every FAST result bitwise independent of the
+  // grid, sharding and batching.
+  bool splitk = true;
 
   static Config defaults() { return Config{}; }
   static Config load(const std::optional<std::string>& file = std::nullopt, bool apply_env = true);
@@ -298,7 +304,8 @@ void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar b
 
 // Runs an already-built plan on device operands (the boundary the reference's
 // dispatch.cpp:359-388 crosses).
-void execute(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc = nullptr);
+void execute(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc = nullptr,
+             bool allow_splitk = true);
 
 // --------------------------------------------------------------- case labels
 struct CaseLabel {

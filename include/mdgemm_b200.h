@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define MDG_ABI_VERSION 1
+#define MDG_ABI_VERSION 2
 
 /* ---- enumerations (values follow the reference enums' declaration order) -- */
 
@@ -65,6 +65,8 @@ enum { MDG_CTEMP_COPY_BACK = 0, MDG_CTEMP_ACCUMULATE_BACK = 1 };
  *          block combine exactly as gemm_blocked does): bitwise identical to
  *          the reference CPU engine for the same Config. */
 enum { MDG_NUMERICS_FAST = 0, MDG_NUMERICS_EXACT = 1 };
+/* mdg_execute: OR into `numerics` to forbid split-K for this call */
+enum { MDG_EXEC_NO_SPLITK = 0x100 };
 
 /* Status codes */
 enum { MDG_OK = 0, MDG_ERR = 1, MDG_ERR_SCALAR_POLICY = 2, MDG_ERR_CUDA = 3 };
@@ -102,6 +104,8 @@ typedef struct mdg_config {
   int32_t preference;
   int32_t ctemp;
   int32_t numerics;
+  int32_t splitk;    /* gpu.splitk: 1 auto (default), 0 off */
+  int32_t reserved;
 } mdg_config_t;
 
 /* ExecutionPlan (dispatch.hpp:52-80) */
@@ -251,6 +255,13 @@ typedef struct mdg_kernel_stats {
   double total_ms;
   double work;
 } mdg_kernel_stats_t;
+
+/* Workspace: the library allocates packed panels, staged host operands and
+ * C_temp-style scratch from its own stream-ordered pool per device, which
+ * keeps what it has between calls (no mapping inside a batch).  This
+ * synchronises the current device and returns the pool's memory above
+ * keep_bytes to the system. */
+int mdg_trim_workspace(uint64_t keep_bytes);
 
 uint64_t mdg_launch_count(void);
 /* Bytes the batch runner has staged host->device / device->host so far. */

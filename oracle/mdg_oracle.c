@@ -149,6 +149,7 @@ int orc_config_defaults(mdg_config_t* o) { /* config.hpp:38-41 */
   o->preference = MDG_PREF_COLUMN;
   o->ctemp = MDG_CTEMP_AUTO;
   o->numerics = MDG_NUMERICS_FAST;
+  o->splitk = 1;
   return MDG_OK;
 }
 

@@ -6,7 +6,9 @@
 
 Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs may
 import this module, and only as the checker.  Both libraries take HOST
-pointers and the same plain-data structs as the product ABI.
+pointers and the same plain-data structs as the product ABI; the structs are
+declared in oracle/abi.py (this module never imports the product package),
+and the wrappers below accept the product's same-layout ctypes structs too.
 """
 from __future__ import annotations
 
@@ -14,8 +16,8 @@ import ctypes
 import os
 from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
-from paper_1901_06015_b200 import (ERR, ERR_SCALAR_POLICY, OK, Config, Error, ExecutionPlan, MatrixView, Scalar,
-                                   ScalarPolicyError)
+from oracle.abi import (ERR_SCALAR_POLICY, OK, Config, Error, ExecutionPlan, MatrixView, Scalar, ScalarPolicyError,
+                        convert)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libmdg_oracle.so")
@@ -93,60 +95,88 @@ def check_ref(rc: int) -> None:
 
 
 # ------------------------------------------------------------ convenience
+def _args(alpha, a, b, beta, c, cfg):
+    return (convert(Scalar, alpha), convert(MatrixView, a), convert(MatrixView, b), convert(Scalar, beta),
+            convert(MatrixView, c), convert(Config, cfg))
+
+
+def orc_config_defaults() -> Config:
+    out = Config()
+    check_orc(orc.orc_config_defaults(byref(out)))
+    return out
+
+
 def orc_plan(alpha, a, b, beta, c, cfg=None) -> ExecutionPlan:
+    alpha, a, b, beta, c, cfg = _args(alpha, a, b, beta, c, cfg)
     out = ExecutionPlan()
-    check_orc(orc.orc_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(out)))
+    check_orc(orc.orc_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or orc_config_defaults()), byref(out)))
     return out
 
 
 def ref_plan(alpha, a, b, beta, c, cfg=None) -> ExecutionPlan:
+    alpha, a, b, beta, c, cfg = _args(alpha, a, b, beta, c, cfg)
     out = ExecutionPlan()
-    check_ref(ref.ref_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(out)))
+    check_ref(ref.ref_plan(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or orc_config_defaults()), byref(out)))
     return out
 
 
 def orc_gemm(alpha, a, b, beta, c, cfg=None) -> int:
+    alpha, a, b, beta, c, cfg = _args(alpha, a, b, beta, c, cfg)
     flops = c_uint64(0)
-    check_orc(orc.orc_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(flops)))
+    check_orc(orc.orc_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or orc_config_defaults()), byref(flops)))
     return flops.value
 
 
 def ref_gemm(alpha, a, b, beta, c, cfg=None) -> int:
+    alpha, a, b, beta, c, cfg = _args(alpha, a, b, beta, c, cfg)
     flops = c_uint64(0)
-    check_ref(ref.ref_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), byref(flops)))
+    check_ref(ref.ref_gemm(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or orc_config_defaults()), byref(flops)))
     return flops.value
 
 
 def orc_pack(src, side, fmt, conj, scale, target, reg_block, panel_len, dst_ptr) -> None:
+    src, scale = convert(MatrixView, src), convert(Scalar, scale)
     check_orc(orc.orc_pack(byref(src), side, fmt, int(conj), scale, target, reg_block, panel_len, c_void_p(dst_ptr)))
 
 
 def ref_pack(src, side, fmt, conj, scale, target, reg_block, dst_ptr, cap) -> None:
+    src, scale = convert(MatrixView, src), convert(Scalar, scale)
     check_ref(ref.ref_pack(byref(src), side, fmt, int(conj), scale, target, reg_block, c_void_p(dst_ptr), cap))
 
 
 def orc_packed_bytes(src, side, fmt, target, reg_block, panel_len=0) -> int:
+    src = convert(MatrixView, src)
     return orc.orc_packed_bytes(byref(src), side, fmt, target, reg_block, panel_len)
 
 
+def ref_packed_bytes(src, side, fmt, target, reg_block) -> int:
+    return ref.ref_packed_bytes(byref(convert(MatrixView, src)), side, fmt, target, reg_block)
+
+
 def orc_violation(alpha, a, b, beta, c_before, c_after, comp_prec) -> float:
+    alpha, a, b, beta, c_before, _ = _args(alpha, a, b, beta, c_before, None)
+    c_after = convert(MatrixView, c_after)
     v = c_double(0.0)
     check_orc(orc.orc_violation(alpha, byref(a), byref(b), beta, byref(c_before), byref(c_after), comp_prec, byref(v)))
     return v.value
 
 
 def ref_violation(alpha, a, b, beta, c_before, c_after, comp_prec) -> float:
+    alpha, a, b, beta, c_before, _ = _args(alpha, a, b, beta, c_before, None)
+    c_after = convert(MatrixView, c_after)
     v = c_double(0.0)
     check_ref(ref.ref_violation(alpha, byref(a), byref(b), beta, byref(c_before), byref(c_after), comp_prec, byref(v)))
     return v.value
 
 
 def orc_fill_uniform(v, state: int) -> None:
+    v = convert(MatrixView, v)
     check_orc(orc.orc_fill_uniform(byref(v), c_uint64(state)))
 
 
 def ref_fill_uniform_path(v, seed: int, path) -> None:
     """Fill through the reference Rng: Rng(seed).split(p0).split(p1)...; str = tag, int = salt."""
+    v = convert(MatrixView, v)
     n = len(path)
     tags = (c_char_p * max(n, 1))(*[p.encode() if isinstance(p, str) else None for p in path])
     salts = (c_uint64 * max(n, 1))(*[0 if isinstance(p, str) else int(p) for p in path])

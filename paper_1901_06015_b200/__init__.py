@@ -137,7 +137,8 @@ class _Blocking(ctypes.Structure):
 class Config(ctypes.Structure):
     """Config (config.hpp:38-72) plus gpu.numerics = fast | exact."""
     _fields_ = [("single_params", _Blocking), ("double_params", _Blocking), ("threads", c_int32),
-                ("preference", c_int32), ("ctemp", c_int32), ("numerics", c_int32)]
+                ("preference", c_int32), ("ctemp", c_int32), ("numerics", c_int32),
+                ("splitk", c_int32), ("reserved", c_int32)]
 
     @staticmethod
     def defaults() -> "Config":
@@ -259,6 +260,7 @@ def _load() -> ctypes.CDLL:
         "mdg_rng_split_tag": (c_uint64, [c_uint64, c_char_p]),
         "mdg_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
         "mdg_shard_columns": (c_int, [c_int64, c_int32, c_int32, c_int64, POINTER(c_int64), POINTER(c_int64)]),
+        "mdg_trim_workspace": (c_int, [c_uint64]),
         "mdg_launch_count": (c_uint64, []),
         "mdg_staging_bytes": (None, [POINTER(c_uint64), POINTER(c_uint64)]),
         "mdg_profile_begin": (c_int, []),
@@ -278,13 +280,19 @@ EXPORTED_SYMBOLS = (
     "mdg_dual_schedule",
     "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
-    "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
+    "mdg_trim_workspace", "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
 )
 
 
 def launch_count() -> int:
     """Kernels this process has launched through the library."""
     return lib.mdg_launch_count()
+
+
+def trim_workspace(keep_bytes: int = 0) -> None:
+    """Synchronise the device and give the library pool's cached workspace
+    above keep_bytes back to the system."""
+    _check(lib.mdg_trim_workspace(keep_bytes))
 
 
 def staging_bytes() -> tuple[int, int]:

@@ -166,9 +166,10 @@ cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, voi
 inline bool pack_pair_ok(const PackDesc& a, const PackDesc& b) {
   return a.src.dtype == b.src.dtype && a.target_single == b.target_single && a.format == b.format;
 }
-cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s);
-cudaError_t launch_fill_uniform(const DView& v, uint64_t state, cudaStream_t s);
-cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, cudaStream_t s);
+// (sms: the SM count the grid-stride grids are sized for)
+cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, int sms, cudaStream_t s);
+cudaError_t launch_fill_uniform(const DView& v, uint64_t state, int sms, cudaStream_t s);
+cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, int sms, cudaStream_t s);
 
 // Fast kernels: tile shape chosen by the driver.
 struct FastTile {

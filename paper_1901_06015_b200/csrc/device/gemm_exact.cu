@@ -101,12 +101,12 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(GemmDesc d) {
 
 }  // namespace
 
-cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, cudaStream_t s) {
+cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, int sms, cudaStream_t s) {
   const bool prow = d.epi.pair == MDG_PAIR_ROWS, pcol = d.epi.pair == MDG_PAIR_COLS;
   const int64_t total = (prow ? d.me / 2 : d.me) * (pcol ? d.ne / 2 : d.ne);
   if (total == 0) return cudaSuccess;
   int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 64) blocks = 148 * 64;
+  if (blocks > int64_t{sms} * 64) blocks = int64_t{sms} * 64;
   if (single)
     gemm_exact_kernel<float><<<static_cast<unsigned>(blocks), 256, 0, s>>>(d);
   else

@@ -45,22 +45,22 @@ __global__ void fill_uniform_kernel(DView v, uint64_t state) {
   }
 }
 
-int grid_for(int64_t total) {
-  const int64_t blocks = (total + 255) / 256;
-  return static_cast<int>(blocks < 148 * 32 ? (blocks > 0 ? blocks : 1) : 148 * 32);
+int grid_for(int64_t total, int sms) {
+  const int64_t blocks = (total + 255) / 256, cap = int64_t{sms > 0 ? sms : 1} * 32;
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
 }  // namespace
 
-cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, cudaStream_t s) {
+cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, int sms, cudaStream_t s) {
   if (out.m * out.n == 0) return cudaSuccess;
-  beta_pass_kernel<<<grid_for(out.m * out.n), 256, 0, s>>>(out, beta);
+  beta_pass_kernel<<<grid_for(out.m * out.n, sms), 256, 0, s>>>(out, beta);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fill_uniform(const DView& v, uint64_t state, cudaStream_t s) {
+cudaError_t launch_fill_uniform(const DView& v, uint64_t state, int sms, cudaStream_t s) {
   if (v.m * v.n == 0) return cudaSuccess;
-  fill_uniform_kernel<<<grid_for(v.m * v.n), 256, 0, s>>>(v, state);
+  fill_uniform_kernel<<<grid_for(v.m * v.n, sms), 256, 0, s>>>(v, state);
   return cudaGetLastError();
 }
 

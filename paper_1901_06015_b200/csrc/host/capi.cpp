@@ -77,6 +77,7 @@ Config config_from(const mdg_config_t* c) {
   cfg.preference = c->preference == MDG_PREF_ROW ? Preference::Row : Preference::Column;
   cfg.ctemp = c->ctemp == MDG_CTEMP_ON ? CTempMode::On : c->ctemp == MDG_CTEMP_OFF ? CTempMode::Off : CTempMode::Auto;
   cfg.numerics = c->numerics == MDG_NUMERICS_EXACT ? Numerics::Exact : Numerics::Fast;
+  cfg.splitk = c->splitk != 0;
   return cfg;
 }
 
@@ -87,6 +88,8 @@ void config_to(const Config& cfg, mdg_config_t* o) {
   o->preference = cfg.preference == Preference::Row ? MDG_PREF_ROW : MDG_PREF_COLUMN;
   o->ctemp = cfg.ctemp == CTempMode::On ? MDG_CTEMP_ON : cfg.ctemp == CTempMode::Off ? MDG_CTEMP_OFF : MDG_CTEMP_AUTO;
   o->numerics = cfg.numerics == Numerics::Exact ? MDG_NUMERICS_EXACT : MDG_NUMERICS_FAST;
+  o->splitk = cfg.splitk ? 1 : 0;
+  o->reserved = 0;
 }
 
 ExecutionPlan plan_from(const mdg_plan_t* q) {
@@ -266,7 +269,8 @@ int mdg_plan(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b, mdg_s
 int mdg_execute(const mdg_plan_t* p, int32_t numerics, void* stream, uint64_t* flops_out) {
   return guarded([&] {
     FlopCounter fc;
-    execute(plan_from(p), numerics == MDG_NUMERICS_EXACT ? Numerics::Exact : Numerics::Fast, stream, &fc);
+    execute(plan_from(p), (numerics & 0xff) == MDG_NUMERICS_EXACT ? Numerics::Exact : Numerics::Fast, stream, &fc,
+            (numerics & MDG_EXEC_NO_SPLITK) == 0);
     if (flops_out) *flops_out = fc.value();
   });
 }
@@ -360,7 +364,7 @@ int mdg_fill_uniform(const mdg_view_t* v, uint64_t rng_state, void* stream) {
     const MatrixView mv = view_from(v);
     prof::Scope scope(MDG_KERNEL_FILL, static_cast<cudaStream_t>(stream),
                       static_cast<double>(mv.m) * mv.n * dtype_size(mv.dtype));
-    cuda_check(mdg::launch_fill_uniform(to_dview(view_from(v)), rng_state, static_cast<cudaStream_t>(stream)),
+    cuda_check(mdg::launch_fill_uniform(to_dview(view_from(v)), rng_state, device_sms(), static_cast<cudaStream_t>(stream)),
                "fill_uniform");
   });
 }
@@ -382,6 +386,10 @@ int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align, int
     *j0 = lo;
     *nb = std::min<int64_t>(chunk, n - lo);
   });
+}
+
+int mdg_trim_workspace(uint64_t keep_bytes) {
+  return guarded([&] { trim_workspace(static_cast<size_t>(keep_bytes)); });
 }
 
 uint64_t mdg_launch_count(void) { return prof::launches(); }

@@ -17,7 +17,7 @@ namespace mdgemm {
 
 namespace {
 
-int device_sms() {
+int device_sms_impl() {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   static std::mutex mu;
@@ -27,31 +27,79 @@ int device_sms() {
   if (cache[dev] == 0) {
     int sms = 0;
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-    // Keep stream-ordered workspace cached between calls.
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      // Never let an allocation on one compute stream wait for a free on
-      // another (the allocator would insert that dependency to reuse the
-      // block, serialising the concurrent calls of a batch): grow instead.
-      int no = 0;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
-      // Optional up-front reservation (MDGEMM_POOL_RESERVE_GB): growing the
-      // pool maps new memory in the middle of a batch.
-      if (const char* f = std::getenv("MDGEMM_POOL_RESERVE_GB")) {
-        const double gb = std::atof(f);
-        void* p = nullptr;
-        if (gb > 0 && cudaMallocAsync(&p, static_cast<size_t>(gb * (1ull << 30)), cudaStreamLegacy) == cudaSuccess) {
-          cudaFreeAsync(p, cudaStreamLegacy);
-          cudaStreamSynchronize(cudaStreamLegacy);
-        }
-      }
+    // tests only (MDGEMM_SMS): schedule for fewer SMs than the device has, so
+    // that small problems exercise the persistent, stream-K and multi-tile
+    // paths (compute-sanitizer runs)
+    if (const char* f = std::getenv("MDGEMM_SMS")) {
+      const int cap = std::atoi(f);
+      if (cap > 0 && cap < sms) sms = cap;
     }
     cache[dev] = sms;
   }
   return cache[dev];
 }
+
+}  // namespace
+
+int device_sms() { return device_sms_impl(); }
+
+// The library's own stream-ordered pool per device (workspace, staged host
+// operands).  A private pool, not the device's default one: its "keep what
+// you have" release threshold must not change how other users of the
+// default pool in the same process (PyTorch, other libraries) get memory
+// back, and trim_workspace() can hand it all back.
+cudaMemPool_t workspace_pool() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static std::vector<cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  if (pools.size() <= static_cast<size_t>(dev)) pools.resize(dev + 1, nullptr);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    cuda_check(cudaMemPoolCreate(&pool, &props), "cudaMemPoolCreate");
+    // Keep stream-ordered workspace cached between calls (release with
+    // trim_workspace / mdg_trim_workspace).
+    uint64_t keep = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // Never let an allocation on one compute stream wait for a free on
+    // another (the allocator would insert that dependency to reuse the
+    // block, serialising the concurrent calls of a batch): grow instead.
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+    pools[dev] = pool;
+    // Optional up-front reservation (MDGEMM_POOL_RESERVE_GB): growing the
+    // pool maps new memory in the middle of a batch.
+    if (const char* f = std::getenv("MDGEMM_POOL_RESERVE_GB")) {
+      const double gb = std::atof(f);
+      void* p = nullptr;
+      if (gb > 0 && cudaMallocFromPoolAsync(&p, static_cast<size_t>(gb * (1ull << 30)), pool, cudaStreamLegacy) ==
+                        cudaSuccess) {
+        cudaFreeAsync(p, cudaStreamLegacy);
+        cudaStreamSynchronize(cudaStreamLegacy);
+      }
+      cudaGetLastError();
+    }
+  }
+  return pools[dev];
+}
+
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
+  return cudaMallocFromPoolAsync(p, bytes, workspace_pool(), st);
+}
+
+void trim_workspace(size_t keep_bytes) {
+  cuda_check(cudaDeviceSynchronize(), "trim_workspace: synchronize");
+  cuda_check(cudaMemPoolTrimTo(workspace_pool(), keep_bytes), "cudaMemPoolTrimTo");
+  reset_reservation();
+}
+
+namespace {
 
 int32_t dt_code(Datatype t) {
   return (t.domain == Domain::Complex ? 2 : 0) + (t.precision == Precision::Double ? 1 : 0);
@@ -255,6 +303,9 @@ static int encode_c_map(mdg::DEpilogue& e, int bm, int bn) {
     return mdg::MDG_CMAP_NONE;
   }
   if (stride % 16 || (inner * esr) % 16 || inner > 256) return mdg::MDG_CMAP_NONE;
+  // the kernels pass box coordinates as 32-bit ints: a taller or wider C
+  // takes the element-wise path
+  if (dims[0] > 0x7fffffffull || dims[1] > 0x7fffffffull) return mdg::MDG_CMAP_NONE;
   const cuuint64_t strides[1] = {stride};
   const cuuint32_t box[2] = {inner, static_cast<cuuint32_t>(mdg::C_BOX_COLS)};
   const cuuint32_t estride[2] = {1, 1};
@@ -291,18 +342,18 @@ static int ctas_per_sm(const mdg::FastTile& t, bool single, int cdt) {
   return v;
 }
 
-void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc) {
-  execute_scheduled(p, numerics, stream_ptr, fc, false);
+void execute(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool allow_splitk) {
+  execute_scheduled(p, numerics, stream_ptr, fc, false, nullptr, 0, nullptr, allow_splitk);
 }
 
-size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared) {
+size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, bool allow_splitk) {
   size_t n = 0;
-  execute_scheduled(p, numerics, nullptr, nullptr, shared, nullptr, 0, &n);
+  execute_scheduled(p, numerics, nullptr, nullptr, shared, nullptr, 0, &n, allow_splitk);
   return n;
 }
 
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared,
-                       void* arena, size_t arena_bytes, size_t* ws_needed) {
+                       void* arena, size_t arena_bytes, size_t* ws_needed, bool allow_splitk) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (ws_needed) *ws_needed = 0;
   if (p.m == 0 || p.n == 0) return;
@@ -328,7 +379,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
     if (ws_needed) return;
     if (!p.beta.is_one()) {
       prof::Scope scope(MDG_KERNEL_BETA, st, 2.0 * p.c.m * p.c.n * dtype_size(p.c.dtype));
-      cuda_check(mdg::launch_beta_pass(to_dview(p.c), to_dbeta(p.beta), st), "beta pass");
+      cuda_check(mdg::launch_beta_pass(to_dview(p.c), to_dbeta(p.beta), device_sms(), st), "beta pass");
     }
     return;
   }
@@ -376,7 +427,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   const int64_t tiles = ((p.m + tile.bm - 1) / tile.bm) * ((p.n + tile.bn - 1) / tile.bn);
   const int per_sm = exact || dmma_ws ? 1 : ctas_per_sm(tile, single, to_dview(p.c).dtype);
   const int64_t nk = lpad / tile.bk;
-  int splits = exact || dmma_ws ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
+  int splits = exact || dmma_ws || !allow_splitk ? 1 : mdg::choose_splits(tiles, nk, sms * per_sm);
   int kb_per_split = static_cast<int>(nk);
   if (splits > 1) {
     kb_per_split = static_cast<int>((nk + splits - 1) / splits);
@@ -440,7 +491,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   void* ws = nullptr;
   const bool owned = !(arena && arena_bytes >= off_f + flag_bytes);
   if (owned) {
-    cuda_check(cudaMallocAsync(&ws, off_f + flag_bytes, st), "workspace allocation");
+    cuda_check(ws_alloc(&ws, off_f + flag_bytes, st), "workspace allocation");
   } else {
     ws = arena;
   }
@@ -522,13 +573,13 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
         g.flat = to_dview(real_flatten(p.c, ax));
       }
       prof::Scope scope(MDG_KERNEL_EXACT, st, 2.0 * p.m * p.n * p.k);
-      err = mdg::launch_gemm_exact(g, single, st);
+      err = mdg::launch_gemm_exact(g, single, sms, st);
     } else {
       const int kind = single ? MDG_KERNEL_FFMA : MDG_KERNEL_DMMA;
       const char* trace_path = std::getenv("MDGEMM_TRACE");  // tuning: per-CTA timeline of every gemm kernel
       const int64_t grid = dmma_ws ? ws_grid : sk_grid > 0 ? mdg::sk_launch_grid(tiles, sk_grid) : tiles * splits;
       if (trace_path && grid > 0 && err == cudaSuccess)
-        err = cudaMallocAsync(reinterpret_cast<void**>(&g.trace), grid * mdg::TRACE_WORDS * 8, st);
+        err = ws_alloc(reinterpret_cast<void**>(&g.trace), grid * mdg::TRACE_WORDS * 8, st);
       {
         prof::Scope scope(kind, st, 2.0 * p.m * p.n * p.k);
         if (err == cudaSuccess)

@@ -19,6 +19,19 @@ struct CudaFailure : Error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// SMs the kernels are scheduled for (the device's count, or MDGEMM_SMS when
+// a test caps it).
+int device_sms();
+// The library's private stream-ordered pool on the current device, and a
+// stream-ordered allocation from it (free with cudaFreeAsync).
+cudaMemPool_t workspace_pool();
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st);
+// Synchronise the device and return the pool's cached memory above
+// keep_bytes to the system (mdg_trim_workspace).
+void trim_workspace(size_t keep_bytes);
+// Forget the batch reservation (the pool was trimmed).
+void reset_reservation();
+
 mdg::DView to_dview(const MatrixView& v);
 
 // resolve_geometry (packing.cpp:27-67) plus an optional padded panel length.
@@ -49,8 +62,9 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
 // stream).  `ws_needed` (optional): only report the workspace bytes the call
 // would use, launching nothing.
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared,
-                       void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr);
-size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared);
+                       void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr,
+                       bool allow_splitk = true);
+size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, bool allow_splitk = true);
 
 // ---- the dual-pipe kernel (gemm_dual.cu), used by gemm_batch -------------
 // FAST plans it can run: k > 0, non-empty, complex C paired.

@@ -139,12 +139,23 @@ size_t unique_host_bytes(std::vector<Window> w) {
 // resident host windows.  Growing it inside the batch maps memory while
 // calls are being enqueued, which stalled whole steps of the cfg2 sweep by
 // 200-350 ms (measured).  Returns the byte budget for residents.
+namespace {
+std::mutex g_reserve_mu;
+std::vector<size_t> g_reserved;  // bytes the library's pool holds per device
+}  // namespace
+
+void reset_reservation_impl() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_reserve_mu);
+  if (g_reserved.size() > static_cast<size_t>(dev)) g_reserved[dev] = 0;
+}
+
 size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  static std::mutex mu;
-  static std::vector<size_t> reserved;
-  std::lock_guard<std::mutex> lock(mu);
+  std::lock_guard<std::mutex> lock(g_reserve_mu);
+  std::vector<size_t>& reserved = g_reserved;
   if (reserved.size() <= static_cast<size_t>(dev)) reserved.resize(dev + 1, 0);
   // Device operands only and the pool already holds the arenas: nothing to
   // decide (and no cudaMemGetInfo, which stalled lone-call enqueues)
@@ -158,12 +169,9 @@ size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
   if (const char* f = std::getenv("MDGEMM_RESIDENT_MB"))  // tests: force evictions
     budget = std::min(budget, static_cast<size_t>(std::atof(f) * (1 << 20)));
   const size_t want = arenas + std::min(host_bytes, budget);
-  cudaMemPool_t pool;
-  if (want == 0 || want <= reserved[dev] || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return budget;
-  uint64_t keep = ~0ULL;  // the pool must keep what is reserved (driver.cpp sets the same)
-  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  void* ptr = nullptr;
-  if (cudaMallocAsync(&ptr, want, cudaStreamLegacy) == cudaSuccess) {
+  if (want == 0 || want <= reserved[dev]) return budget;
+  void* ptr = nullptr;  // the library's pool keeps what is reserved (driver.cpp: workspace_pool)
+  if (ws_alloc(&ptr, want, cudaStreamLegacy) == cudaSuccess) {
     cudaFreeAsync(ptr, cudaStreamLegacy);  // the pool keeps it (release threshold: never)
     reserved[dev] = want;
   }
@@ -553,7 +561,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
     residents.resize(all.size());
     for (size_t x : order) {
       void* d = nullptr;
-      cuda_check(cudaMallocAsync(&d, all[x].bytes(), S.in), "staging allocation");
+      cuda_check(ws_alloc(&d, all[x].bytes(), S.in), "staging allocation");
       residents[x] = {all[x], static_cast<std::byte*>(d)};
       cuda_check(cudaMemcpyAsync(d, all[x].lo, all[x].bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
       g_h2d_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
@@ -585,7 +593,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
     };
     for (size_t i = 0; i < n; ++i) rebase(i);
     if (arena_bytes > 0)
-      for (void*& a : arena) cuda_check(cudaMallocAsync(&a, arena_bytes, P), "workspace allocation");
+      for (void*& a : arena) cuda_check(ws_alloc(&a, arena_bytes, P), "workspace allocation");
     // per-launch tile counters of the dynamic tile order (MDGEMM_DUAL_DYNAMIC=1; the
     // default static boustrophedon order measured 0.7 % faster on the cfg2 sweep: the
     // atomic fetch at every tile start delays the producer's first copies)
@@ -594,7 +602,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
       return f ? std::atoi(f) != 0 : false;
     }();
     if (dynamic && !units.empty()) {
-      cuda_check(cudaMallocAsync(&counters, units.size() * 2 * sizeof(int), K), "tile counters");
+      cuda_check(ws_alloc(reinterpret_cast<void**>(&counters), units.size() * 2 * sizeof(int), K), "tile counters");
       cuda_check(cudaMemsetAsync(counters, 0, units.size() * 2 * sizeof(int), K), "tile counters");
     }
     std::vector<cudaEvent_t> k_done(units.size(), nullptr);
@@ -616,7 +624,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
       if (u.classic < 0) wait_inputs(members, true);
       if (u.classic >= 0) {
         Call& c = cs[static_cast<size_t>(u.classic)];
-        execute_scheduled(c.plan, cfg.numerics, K, fc, true);
+        execute_scheduled(c.plan, cfg.numerics, K, fc, true, nullptr, 0, nullptr, cfg.splitk);
       } else {
         // packs: after the kernel that last used this arena and after writers of the A/B read
         if (ui >= 2 && k_done[ui - 2]) cuda_check(cudaStreamWaitEvent(P, k_done[ui - 2], 0), "arena reuse");
@@ -803,7 +811,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
   // the largest call, instead of a pool allocation per call.
   const bool shared = cs.size() > 1;
   size_t arena_want = 0;
-  for (const Call& c : cs) arena_want = std::max(arena_want, workspace_bytes(c.plan, cfg.numerics, shared));
+  for (const Call& c : cs) arena_want = std::max(arena_want, workspace_bytes(c.plan, cfg.numerics, shared, cfg.splitk));
   const size_t budget = reserve_for_batch(unique_host_bytes(host_windows), arena_want,
                                           std::min<int>(nstreams, static_cast<int>(cs.size())));
   void* arena[kComputeStreams] = {};
@@ -920,7 +928,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
         Resident nr;
         nr.host = h;
         void* d = nullptr;
-        cuda_check(cudaMallocAsync(&d, h.bytes(), S.in), "staging allocation");
+        cuda_check(ws_alloc(&d, h.bytes(), S.in), "staging allocation");
         nr.dev = static_cast<std::byte*>(d);
         cuda_check(cudaMemcpyAsync(d, h.lo, h.bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
         g_h2d_bytes.fetch_add(h.bytes(), std::memory_order_relaxed);
@@ -1004,7 +1012,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
 
       // (the planning-time size saw host operand addresses; a staged call's
       // tensor-map alignment can differ, so re-check and grow in stream order)
-      const size_t ws_need = c.active ? workspace_bytes(p, cfg.numerics, shared) : 0;
+      const size_t ws_need = c.active ? workspace_bytes(p, cfg.numerics, shared, cfg.splitk) : 0;
       if (ws_need > arena_size[c.stream]) {
         if (arena[c.stream]) {
           cuda_check(cudaFreeAsync(arena[c.stream], cst), "workspace release");
@@ -1012,10 +1020,10 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
           arena_size[c.stream] = 0;
         }
         const size_t bytes = std::max(ws_need, arena_want);
-        cuda_check(cudaMallocAsync(&arena[c.stream], bytes, cst), "workspace allocation");
+        cuda_check(ws_alloc(&arena[c.stream], bytes, cst), "workspace allocation");
         arena_size[c.stream] = bytes;
       }
-      execute_scheduled(p, cfg.numerics, cst, fc, shared, arena[c.stream], arena_size[c.stream]);
+      execute_scheduled(p, cfg.numerics, cst, fc, shared, arena[c.stream], arena_size[c.stream], nullptr, cfg.splitk);
       cuda_check(cudaEventRecord(c.comp_done, cst), "event");
       for (size_t e : mine) res[e].last_use[c.stream] = static_cast<long>(i);
       if (holder[2]) {
@@ -1103,7 +1111,7 @@ void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar b
                 const Config& cfg, void* stream, FlopCounter* fc) {
   if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
   const ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
-  execute(p, cfg.numerics, stream, fc);
+  execute(p, cfg.numerics, stream, fc, cfg.splitk);
 }
 
 void gemm_batch(const std::vector<GemmCall>& calls, const Config& cfg, FlopCounter* fc) {
@@ -1118,5 +1126,7 @@ void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, c
           const Config& cfg, FlopCounter* fc) {
   gemm_batch({GemmCall{alpha, a, b, beta, c}}, cfg, fc);
 }
+
+void reset_reservation() { reset_reservation_impl(); }
 
 }  // namespace mdgemm

@@ -72,7 +72,7 @@ def main():
     for spec in PACK_SPECS:
         src = pack_input(spec)
         v = src.view(conj=bool(spec["src_conj"]))
-        n = O.ref.ref_packed_bytes(v, spec["side"], spec["fmt"], spec["target"], spec["reg_block"])
+        n = O.ref_packed_bytes(v, spec["side"], spec["fmt"], spec["target"], spec["reg_block"])
         buf = np.zeros(n, np.uint8)
         O.ref_pack(v, spec["side"], spec["fmt"], spec["conj"], SCALARS[spec["scale"]], spec["target"],
                    spec["reg_block"], buf.ctypes.data, n)

@@ -29,10 +29,27 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version_and_struct_sizes():
-    assert M.lib.mdg_abi_version() == 1
+    assert M.lib.mdg_abi_version() == 2  # 2: mdg_config_t gained gpu.splitk
     assert ctypes.sizeof(M.MatrixView) == 56
     assert ctypes.sizeof(M.Scalar) == 24
-    assert ctypes.sizeof(M.Config) == 80
+    assert ctypes.sizeof(M.Config) == 88
+
+
+def test_oracle_abi_mirror_matches_the_product_layout():
+    # the checkers declare the structs themselves (oracle/abi.py), so that the reference
+    # arm never loads the product library: same field names, offsets and sizes
+    from oracle import abi as A
+    for mine, theirs in ((M.MatrixView, A.MatrixView), (M.Scalar, A.Scalar), (M.Config, A.Config),
+                         (M.ExecutionPlan, A.ExecutionPlan)):
+        assert ctypes.sizeof(mine) == ctypes.sizeof(theirs), mine
+        for (name, _), (name2, _) in zip(mine._fields_, theirs._fields_):
+            assert name == name2 and getattr(mine, name).offset == getattr(theirs, name2).offset, (mine, name)
+    for c in (0, 1):
+        for a in (0, 1):
+            for b in (0, 1):
+                label = "dz"[c] + "dz"[a] + "dz"[b] + "d"
+                assert A.case_id(label) == M.classify_case(bool(c), bool(a), bool(b))
+    assert A.flops_of_case(7, 3, 5, 7) == M.flops_of_case(7, 3, 5, 7)
 
 
 def test_config_keys_and_errors():
@@ -41,8 +58,9 @@ def test_config_keys_and_errors():
     cfg.set("gemm.kc.double", 64).set("ukr.preference", "row").set("ctemp.enable", "off").set("gpu.numerics", "exact")
     assert cfg.double_params.kc == 64 and cfg.single_params.kc == 256
     assert (cfg.preference, cfg.ctemp, cfg.numerics) == (M.PREF_ROW, M.CTEMP_OFF, M.EXACT)
+    assert cfg.splitk == 1 and M.Config.defaults().set("gpu.splitk", "off").splitk == 0
     for key, val in (("gemm.bogus", "1"), ("ukr.preference", "diagonal"), ("gemm.kc", "x12"),
-                     ("ctemp.enable", "sometimes"), ("gpu.numerics", "approx")):
+                     ("ctemp.enable", "sometimes"), ("gpu.numerics", "approx"), ("gpu.splitk", "maybe")):
         with pytest.raises(M.Error):
             M.Config.defaults().set(key, val)
     bad = M.Config.defaults().set("ukr.mr", 3)

@@ -62,7 +62,7 @@ def test_scalar_policy_rejections_match_reference():
             try:
                 fn(SCALARS["c55"], va, vb, SCALARS["one"], vc)
                 outcomes.append("ok")
-            except M.ScalarPolicyError:
+            except O.ScalarPolicyError:
                 outcomes.append("policy")
         assert outcomes[0] == outcomes[1], label
         cid = M.CaseLabel.parse(label).case_id()
@@ -90,7 +90,7 @@ def test_pack_matches_reference_bitwise():
             src = HostMatrix(dt, 5, 7, kind).fill(O.orc_rng_state(3, ["pack", dt, side, fmt, kind]))
             v = src.view(conj=src_conj and M.is_complex(dt))
             nbytes = O.orc_packed_bytes(v, side, fmt, target, rb)
-            assert nbytes == O.ref.ref_packed_bytes(v, side, fmt, target, rb)
+            assert nbytes == O.ref_packed_bytes(v, side, fmt, target, rb)
             mine = np.full(nbytes, 0x5A, np.uint8)
             theirs = np.full(nbytes, 0xA5, np.uint8)
             O.orc_pack(v, side, fmt, conj, SCALARS[scale], target, rb, 0, mine.ctypes.data)
@@ -114,9 +114,9 @@ def test_pack_errors_match_reference():
     ]
     buf = np.zeros(4096, np.uint8)
     for v, side, fmt, sc, tgt, rb in bad:
-        with pytest.raises(M.Error):
+        with pytest.raises(O.Error):
             O.orc_pack(v, side, fmt, 0, sc, tgt, rb, 0, buf.ctypes.data)
-        with pytest.raises(M.Error):
+        with pytest.raises(O.Error):
             O.ref_pack(v, side, fmt, 0, sc, tgt, rb, buf.ctypes.data, buf.size)
 
 
