@@ -5,12 +5,14 @@ Metric (BASELINE.json): effective GFLOPS = sum of flops_of_case(label, m, n, k)
 (2/4/8 mnk, dispatch.cpp:35-54) / time, and its fraction of the measured
 FP64-DMMA / FP32-FFMA peak.
 
-Default workload = BASELINE configs[1], the 128-label sweep, at its largest
-size m=n=k=4096: one step runs all 128 cabx labels once with the sweep's
-scalars (alpha = 1.2-0.7i for cases 0 and 3, real 1.2 for the six cases that
-reject a complex alpha; beta = 0.9+0.3i), A/B/C column-major, entries
-uniform[-1,1) from the reference's splitmix64 Rng (generated on the device).
-Other BASELINE configs are available with --workload.
+Default workload = BASELINE configs[1], the full 128-label sweep m=n=k =
+256, 512, ..., 4096: one step runs all 128 cabx labels at all 16 sizes (2,048
+gemm calls, issued as one gemm_batch) with the sweep's scalars (alpha =
+1.2-0.7i for cases 0 and 3, real 1.2 for the six cases that reject a complex
+alpha; beta = 0.9+0.3i), A/B/C column-major, entries uniform[-1,1) from the
+reference's splitmix64 Rng (generated on the device).  Other BASELINE configs
+are available with --workload (cfg5 draws normal(0,1) entries by Box-Muller
+over the same Rng, mdg_fill_normal).
 
 Multi-GPU (torchrun): C and B are split into column panels per rank
 (mdg_shard_columns), A is broadcast from rank 0 over NCCL inside every step;
@@ -117,6 +119,77 @@ def useful_flops(items):
     return sum(M.flops_of_case(M.CaseLabel.parse(l).case_id(), m, n, k) for l, m, n, k, _, _ in items)
 
 
+# ------------------------------------------------------------------ operands
+def make_operands(M, items, workload_name, seed, dist_kind, dev, stream, world=1, rank=0, shard_mode="columns"):
+    """The step's operands and calls: one A/B/C per distinct (role, dtype, shape), so calls with the
+    same C dtype and shape update one C buffer in sequence (a dependency chain), B and C column
+    panels per rank.  Entries from the reference Rng on the device: uniform[-1,1) (fill_uniform) or
+    normal(0,1) by Box-Muller over the same draws (fill_normal).  Shared with the parity test of the
+    bench's own batch (tests/test_bench_parity_gpu.py).
+    Returns (ops {key: (tensor, view)}, shard {item: (j0, nb)}, calls, call_info, a_bufs)."""
+    import torch
+
+    def alloc(dtype, m, n):
+        t = torch.empty(max(m * n, 1) * M.dtype_size(dtype), dtype=torch.uint8, device=dev)
+        return t, M.MatrixView.make(t.data_ptr(), m, n, 1, max(m, 1), dtype)
+
+    ops, a_bufs, shard = {}, [], {}
+    # Multi-GPU split.  chains: every call stays whole; the calls updating one C buffer (a
+    # dependency chain) go to one rank, chains balanced over the ranks by their flops (longest
+    # first); each rank generates the operands it reads.  columns: C and B column panels per
+    # rank, A broadcast from rank 0 inside every step.
+    mine = set()
+    if shard_mode == "chains":
+        chain_flops = {}
+        for lab, m, n, k, _, _ in items:
+            key = (lab[0], m, n)
+            chain_flops[key] = chain_flops.get(key, 0.0) + M.flops_of_case(M.CaseLabel.parse(lab).case_id(), m, n, k)
+        load = [0.0] * world
+        owner = {}
+        for key in sorted(chain_flops, key=lambda x: -chain_flops[x]):
+            r = min(range(world), key=lambda q: load[q])
+            owner[key] = r
+            load[r] += chain_flops[key]
+        mine = {key for key, r in owner.items() if r == rank}
+    for lab, m, n, k, _, _ in items:
+        if shard_mode == "chains":
+            j0, nb = (0, n) if (lab[0], m, n) in mine else (0, 0)
+        else:
+            j0, nb = M.shard_columns(n, world, rank, 128)
+        shard[(lab, m, n, k)] = (j0, nb)
+        if nb == 0:
+            continue
+        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
+        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, nb)), ("c", dc, (m, nb))):
+            key = (role, dt, shape)
+            if key not in ops:
+                t, v = alloc(dt, *shape)
+                tag = f"{workload_name}/{role}/{M.dtype_letter(dt)}/{shape}/r{0 if role == 'a' or shard_mode == 'chains' else rank}"
+                state = M.Rng(seed).split(tag).state
+                if dist_kind == "normal":
+                    M.fill_normal(v, state, stream)
+                else:
+                    M.fill_uniform(v, state, stream)
+                ops[key] = (t, v)
+                if role == "a" and shard_mode == "columns":
+                    a_bufs.append(t)
+    calls, call_info = [], []  # call_info: (case id, useful flops, computation precision) per call
+    for lab, m, n, k, al, be in items:
+        j0, nb = shard[(lab, m, n, k)]
+        if nb == 0:
+            continue
+        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
+        comp = M.SINGLE if lab[3] == "s" else M.DOUBLE
+        va = ops[("a", da, (m, k))][1]
+        vb = ops[("b", db, (k, nb))][1]
+        vc = ops[("c", dc, (m, nb))][1].with_comp_prec(comp)
+        calls.append((al, va, vb, be, vc))
+        cid = M.CaseLabel.parse(lab).case_id()
+        call_info.append((cid, M.flops_of_case(cid, m, nb, k), lab[3]))
+    return ops, shard, calls, call_info, a_bufs
+
+
+
 # ------------------------------------------------------------------- clocks
 # nvidia-smi's NVML queries hold the driver lock: at a 200 ms period they stalled the host
 # enqueue of lone calls by 15-65 ms in 2 of 10 steps (cfg3 33.1 -> 35.3 TFLOP/s at 1000 ms)
@@ -197,72 +270,11 @@ def run_b200(args):
     desc, items, dist_kind = workload(args)
     cfg = M.Config.defaults().set("gpu.numerics", args.numerics)
 
-    # ---- operands: one A/B/C per distinct (role, dtype, shape); B, C column panels per rank
-    def alloc(dtype, m, n):
-        t = torch.empty(max(m * n, 1) * M.dtype_size(dtype), dtype=torch.uint8, device=dev)
-        return t, M.MatrixView.make(t.data_ptr(), m, n, 1, max(m, 1), dtype)
-
-    ops = {}
-    a_bufs = []
-    shard = {}
-    # Multi-GPU split.  chains: every call stays whole; the calls updating one C buffer (a
-    # dependency chain) go to one rank, chains balanced over the ranks by their flops (longest
-    # first); each rank generates the operands it reads.  columns: C and B column panels per
-    # rank, A broadcast from rank 0 inside every step.
     shard_mode = args.shard if args.shard != "auto" else ("chains" if args.workload == "sweep" else "columns")
     if world == 1:
         shard_mode = "columns"
-    mine = set()
-    if shard_mode == "chains":
-        chain_flops = {}
-        for lab, m, n, k, _, _ in items:
-            key = (lab[0], m, n)
-            chain_flops[key] = chain_flops.get(key, 0.0) + M.flops_of_case(M.CaseLabel.parse(lab).case_id(), m, n, k)
-        load = [0.0] * world
-        owner = {}
-        for key in sorted(chain_flops, key=lambda x: -chain_flops[x]):
-            r = min(range(world), key=lambda q: load[q])
-            owner[key] = r
-            load[r] += chain_flops[key]
-        mine = {key for key, r in owner.items() if r == rank}
-    for lab, m, n, k, _, _ in items:
-        if shard_mode == "chains":
-            j0, nb = (0, n) if (lab[0], m, n) in mine else (0, 0)
-        else:
-            j0, nb = M.shard_columns(n, world, rank, 128)
-        shard[(lab, m, n, k)] = (j0, nb)
-        if nb == 0:
-            continue
-        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
-        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, nb)), ("c", dc, (m, nb))):
-            key = (role, dt, shape)
-            if key not in ops:
-                t, v = alloc(dt, *shape)
-                tag = f"{args.workload}/{role}/{M.dtype_letter(dt)}/{shape}/r{0 if role == 'a' or shard_mode == 'chains' else rank}"
-                if dist_kind == "normal":  # normal(0,1) per real component, seeded per operand
-                    g = torch.Generator(device=dev).manual_seed(len(ops) * 7919 + 13 * (rank if role != "a" else 0))
-                    real = torch.float32 if M.precision_of(dt) == M.SINGLE else torch.float64
-                    flat = t.view(real)
-                    flat.copy_(torch.randn(flat.numel(), generator=g, device=dev, dtype=real))
-                else:
-                    M.fill_uniform(v, M.Rng(args.seed).split(tag).state, stream)
-                ops[key] = (t, v)
-                if role == "a" and shard_mode == "columns":
-                    a_bufs.append(t)
-    calls, call_info = [], []  # call_info: (case id, useful flops, computation precision) per call
-    for lab, m, n, k, al, be in items:
-        j0, nb = shard[(lab, m, n, k)]
-        dc, da, db = (M.dtype_from_letter(ch) for ch in lab[:3])
-        comp = M.SINGLE if lab[3] == "s" else M.DOUBLE
-        if nb == 0:
-            continue
-        va = ops[("a", da, (m, k))][1]
-        vb = ops[("b", db, (k, nb))][1]
-        vc = ops[("c", dc, (m, nb))][1].with_comp_prec(comp)
-        if nb > 0:
-            calls.append((al, va, vb, be, vc))
-            cid = M.CaseLabel.parse(lab).case_id()
-            call_info.append((cid, M.flops_of_case(cid, m, nb, k), lab[3]))
+    ops, shard, calls, call_info, a_bufs = make_operands(M, items, args.workload, args.seed, dist_kind, dev, stream,
+                                                         world, rank, shard_mode)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     def step():
@@ -493,7 +505,8 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (per label computation precision)",
         "data": "synthetic: reference splitmix64 Rng uniform[-1,1) generated on device"
-                if dist_kind == "uniform" else "synthetic: normal(0,1) from a seeded device generator",
+                if dist_kind == "uniform" else
+                "synthetic: normal(0,1) by Box-Muller over the reference splitmix64 Rng draws (mdg_fill_normal), on device",
         "config": {"workload": desc, "calls": len(items), "labels": len({it[0] for it in items}),
                    "numerics": args.numerics,
                    "parallelism": ("single GPU" if world == 1 else

@@ -223,6 +223,10 @@ int mdg_pack_operand(const mdg_view_t* src, int32_t side, int32_t format, int32_
  * stream with state `rng_state`, so device inputs equal the reference's
  * seeded host inputs bit for bit. */
 int mdg_fill_uniform(const mdg_view_t* v, uint64_t rng_state, void* stream);
+/* normal(0,1) entries from the same stream (BASELINE configs[4]; the
+ * reference has no normal generator): Box-Muller, real component t from draws
+ * 2t and 2t+1: u1 = (1 - d0)/2, u2 = (1 + d1)/2, z = sqrt(-2 ln u1) cos(2 pi u2). */
+int mdg_fill_normal(const mdg_view_t* v, uint64_t rng_state, void* stream);
 
 /* Rng::split(tag) / Rng::split(salt) (rng.hpp:34-41) on a raw state. */
 uint64_t mdg_rng_split_tag(uint64_t state, const char* tag);

@@ -16,6 +16,8 @@ import ctypes
 import os
 from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_uint64, c_void_p
 
+import numpy as np
+
 from oracle.abi import (ERR_SCALAR_POLICY, OK, Config, Error, ExecutionPlan, MatrixView, Scalar, ScalarPolicyError,
                         convert)
 
@@ -188,3 +190,36 @@ def orc_rng_state(seed: int, path) -> int:
     for p in path:
         s = orc.orc_rng_split_tag(s, p.encode()) if isinstance(p, str) else orc.orc_rng_split_salt(s, int(p))
     return s
+
+
+# ------------------------------------------------------ reference Rng draws (numpy)
+_GAMMA = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _mix(z):
+    """Rng::mix (rng.hpp:17-22) on a uint64 array (wrapping arithmetic)."""
+    z = z + _GAMMA
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def uniform_draws(state: int, t) -> np.ndarray:
+    """Draw t (0-based) of the stream with state s: next_uniform after t+1 steps
+    (rng.hpp:24-31): 2 * ((mix(s + (t+1) gamma) >> 11) * 2^-53) - 1."""
+    t = np.asarray(t, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = _mix(np.uint64(state) + (t + np.uint64(1)) * _GAMMA)
+    return 2.0 * ((x >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) - 1.0
+
+
+def normal_values(state: int, t) -> np.ndarray:
+    """Box-Muller normal(0,1) of real component t (mdg_fill_normal's definition;
+    the reference has no normal generator): draws 2t and 2t+1,
+    u1 = (1 - d0)/2 in (0, 1], u2 = (1 + d1)/2, z = sqrt(-2 ln u1) cos(2 pi u2).
+    Host libm and the device's log/cospi may differ in the last bits; parity
+    tests feed the oracle the device's bytes."""
+    t = np.asarray(t, dtype=np.uint64)
+    u1 = 0.5 * (1.0 - uniform_draws(state, 2 * t))
+    u2 = 0.5 * (1.0 + uniform_draws(state, 2 * t + np.uint64(1)))
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)

@@ -17,7 +17,7 @@ from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, 
 
 __all__ = [
     "Error", "ScalarPolicyError", "CudaError", "lib", "MatrixView", "Scalar", "Config", "ExecutionPlan",
-    "plan", "gemm", "gemm_batch", "gemm_async", "execute", "pack_block_device", "packed_bytes", "fill_uniform",
+    "plan", "gemm", "gemm_batch", "gemm_async", "execute", "pack_block_device", "packed_bytes", "fill_uniform", "fill_normal",
     "Rng", "classify_case", "flops_of_case", "apply_scalar_policy", "shard_columns", "CaseLabel",
     "DT_S", "DT_D", "DT_C", "DT_Z", "SINGLE", "DOUBLE", "LEFT", "RIGHT", "STANDARD", "ONE_E", "ONE_R",
     "FAST", "EXACT", "dtype_from_letter", "dtype_letter", "dtype_size", "is_complex", "precision_of",
@@ -257,6 +257,7 @@ def _load() -> ctypes.CDLL:
         "mdg_packed_bytes": (c_size_t, [V, c_int32, c_int32, c_int32, c_int64, c_int64]),
         "mdg_pack_operand": (c_int, [V, c_int32, c_int32, c_int32, S, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
         "mdg_fill_uniform": (c_int, [V, c_uint64, c_void_p]),
+        "mdg_fill_normal": (c_int, [V, c_uint64, c_void_p]),
         "mdg_rng_split_tag": (c_uint64, [c_uint64, c_char_p]),
         "mdg_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
         "mdg_shard_columns": (c_int, [c_int64, c_int32, c_int32, c_int64, POINTER(c_int64), POINTER(c_int64)]),
@@ -279,7 +280,7 @@ EXPORTED_SYMBOLS = (
     "mdg_plan", "mdg_execute", "mdg_gemm", "mdg_gemm_batch", "mdg_gemm_batch_async", "mdg_gemm_async",
     "mdg_dual_schedule",
     "mdg_packed_bytes", "mdg_pack_operand",
-    "mdg_fill_uniform", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
+    "mdg_fill_uniform", "mdg_fill_normal", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
     "mdg_trim_workspace", "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
 )
 
@@ -428,6 +429,11 @@ def pack_block_device(dst: int, src: MatrixView, side: int, fmt: int, conj: bool
 
 def fill_uniform(v: MatrixView, state: int, stream=None) -> None:
     _check(lib.mdg_fill_uniform(byref(v), c_uint64(state), _stream_ptr(stream)))
+
+
+def fill_normal(v: MatrixView, state: int, stream=None) -> None:
+    """normal(0,1) entries by Box-Muller over the reference Rng's draws (mdg_fill_normal)."""
+    _check(lib.mdg_fill_normal(byref(v), c_uint64(state), _stream_ptr(stream)))
 
 
 def shard_columns(n: int, world: int, rank: int, align: int = 1) -> tuple[int, int]:

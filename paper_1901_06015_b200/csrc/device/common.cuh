@@ -219,15 +219,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Producer / mover / epilogue-side waits: suspend instead of spinning (see
+// mbar_wait_sleep_u32); the math warps' stage waits keep spinning
+// (mbar_wait_u32).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "n"(20000)
       : "memory");
 }
 
@@ -242,6 +245,22 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
       "r"(parity)
+      : "memory");
+}
+// Wait with a suspend-time hint: a thread whose phase is not complete is
+// suspended (woken when the phase completes, or after `ns`) instead of
+// spinning try_wait / branch / yield.  For waiters that share SM
+// sub-partitions with math warps (the dual kernel's producer lanes spun on
+// their empty barriers for a third of one sub-partition's issue slots).
+__device__ __forceinline__ void mbar_wait_sleep_u32(uint32_t bar, uint32_t parity, uint32_t ns) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(ns)
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {

@@ -169,6 +169,7 @@ inline bool pack_pair_ok(const PackDesc& a, const PackDesc& b) {
 // (sms: the SM count the grid-stride grids are sized for)
 cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, int sms, cudaStream_t s);
 cudaError_t launch_fill_uniform(const DView& v, uint64_t state, int sms, cudaStream_t s);
+cudaError_t launch_fill_normal(const DView& v, uint64_t state, int sms, cudaStream_t s);
 cudaError_t launch_gemm_exact(const GemmDesc& d, bool single, int sms, cudaStream_t s);
 
 // Fast kernels: tile shape chosen by the driver.

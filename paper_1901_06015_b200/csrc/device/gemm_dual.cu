@@ -46,18 +46,40 @@ constexpr int DU_BK = DUAL_BK;      // D group k-block
 constexpr int DF_BK = DUAL_F_BK;    // F group k-block
 constexpr int DD_BM = 128, DD_BN = 128;  // D tile; 8 warps (2 x 4) of 64x32
 constexpr int DF_BM = 64, DF_BN = 128;   // F tile; 128 threads (8 x 16) of 8x8
-constexpr int DD_SA = DU_BK * DD_BM, DD_SB = DU_BK * DD_BN;  // doubles per stage
+// D stages hold each 128-double k-line at a pitch of 132: a DMMA fragment
+// load (lane g + 4 tig reads line kk + tig, element 8i + g) then covers all
+// 32 banks of a half-warp once.  With the packed pitch of 128 the four tig
+// lines of a half-warp fall on the same banks (4-way conflicts; ncu: 48 % of
+// the shared-load wavefronts of the step were conflicts).
+constexpr int DD_P = DD_BM + 4;
+static_assert(DD_BM == DD_BN, "one line pitch for both D operands");
+constexpr int DD_SA = DU_BK * DD_P, DD_SB = DU_BK * DD_P;  // doubles per stage (padded lines)
 constexpr int DF_SA = DF_BK * DF_BM, DF_SB = DF_BK * DF_BN;  // floats per stage
+constexpr int DD_WARPS = 8, DF_WARPS = 4;
 template <int DD_STAGES, int DF_STAGES>
 struct DuRings {
   static constexpr size_t DD_RING = size_t(DD_STAGES) * (DD_SA + DD_SB) * sizeof(double);
   static constexpr size_t DF_RING = size_t(DF_STAGES) * (DF_SA + DF_SB) * sizeof(float);
   static constexpr size_t SMEM =
-      DD_RING + DF_RING + (2 * DD_STAGES + 2 * DF_STAGES) * sizeof(uint64_t) + (DD_STAGES + DF_STAGES) * sizeof(int);
+      DD_RING + DF_RING + (2 * DD_STAGES + 2 * DF_STAGES) * sizeof(uint64_t) + (DD_STAGES + DF_STAGES + DD_WARPS + DF_WARPS) * sizeof(int);
 };
 constexpr int DU_THREADS = 512;
-constexpr int DD_WARPS = 8, DF_WARPS = 4;
+constexpr uint32_t kSleepNs = 20000;  // suspend-time hint of the producers' empty-slot waits
 constexpr int DD_PROD_WARP = 12, DF_PROD_WARP = 13;
+
+// %laneid == 0, read where it is needed (ptxas otherwise keeps `lane` live
+// through the mainloops and spills it at the groups' register caps)
+__device__ __forceinline__ bool lane0() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l == 0;
+}
+
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
 
 __device__ __forceinline__ void dmma884_du(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -277,6 +299,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   uint64_t* fempty = ffull + DF_STAGES;
   int* dslot = reinterpret_cast<int*>(fempty + DF_STAGES);  // tile of each stage's first k-block
   int* fslot = dslot + DD_STAGES;
+  int* dtile = fslot + DF_STAGES;  // D warps: the tile of the running mainloop
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = static_cast<int>(gridDim.x);
   if (threadIdx.x == 0) {
@@ -301,9 +324,11 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     // first, so CTAs that finish early take the next longest: balanced tails),
     // else the static boustrophedon rounds.  The producer hands the tile to
     // its consumers in the first stage's slot; -1 ends the list.
+    // P: smem line pitch of a stage (elements); P == BM: one copy per operand
+    // and stage, else one copy per k-line into padded lines
     auto run_producer = [&](auto* A, auto* B, uint64_t* full, uint64_t* empty, int* slot, const DualJob* jobs,
                             int njobs, int tiles, int* counter, int STAGES, int BM, int BN, int SA, int SB, int BK,
-                            int esz) {
+                            int P, int esz) {
       using T = typename std::remove_pointer<decltype(A)>::type;
       int it = 0;
       auto next = [&](int r) -> int {
@@ -320,7 +345,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         const int v = next(r);
         if (v >= tiles) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
           slot[s] = -1;
           mbar_arrive(&full[s]);
           return;
@@ -334,15 +359,25 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         const int nk = static_cast<int>(jb.lpad / BK);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-          if (kb == 0) slot[s] = v;
-          mbar_arrive_expect_tx(&full[s], (SA + SB) * esz);
-          bulk_g2s(A + s * SA, Ag + static_cast<int64_t>(kb) * SA, SA * esz, &full[s]);
-          bulk_g2s(B + s * SB, Bg + static_cast<int64_t>(kb) * SB, SB * esz, &full[s]);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
+          // stage word: the tile (2v) on its first k-block, bit 0 on its last
+          slot[s] = (kb == 0 ? 2 * v : 0) | (kb == nk - 1 ? 1 : 0);
+          mbar_arrive_expect_tx(&full[s], (BM + BN) * BK * esz);
+          const T* ak = Ag + static_cast<int64_t>(kb) * BK * BM;
+          const T* bk = Bg + static_cast<int64_t>(kb) * BK * BN;
+          if (P == BM) {
+            bulk_g2s(A + s * SA, ak, BK * BM * esz, &full[s]);
+            bulk_g2s(B + s * SB, bk, BK * BN * esz, &full[s]);
+          } else {
+            for (int l = 0; l < BK; ++l) {
+              bulk_g2s(A + s * SA + l * P, ak + l * BM, BM * esz, &full[s]);
+              bulk_g2s(B + s * SB + l * P, bk + l * BN, BN * esz, &full[s]);
+            }
+          }
         }
         if (!counter && (r + 1) * G >= tiles) {  // static order: done after the last round
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
           slot[s] = -1;
           mbar_arrive(&full[s]);
           return;
@@ -351,10 +386,10 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     };
     if (warp == DD_PROD_WARP)
       run_producer(dA, dB, dfull, dempty, dslot, d.d, d.nd, d.tiles_d, d.counters ? d.counters : nullptr, DD_STAGES,
-                   DD_BM, DD_BN, DD_SA, DD_SB, DU_BK, static_cast<int>(sizeof(double)));
+                   DD_BM, DD_BN, DD_SA, DD_SB, DU_BK, DD_P, static_cast<int>(sizeof(double)));
     else if (warp == DF_PROD_WARP)
       run_producer(fA, fB, ffull, fempty, fslot, d.f, d.nf, d.tiles_f, d.counters ? d.counters + 1 : nullptr,
-                   DF_STAGES, DF_BM, DF_BN, DF_SA, DF_SB, DF_BK, static_cast<int>(sizeof(float)));
+                   DF_STAGES, DF_BM, DF_BN, DF_SA, DF_SB, DF_BK, DF_BM, static_cast<int>(sizeof(float)));
     return;
   }
 
@@ -362,38 +397,40 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(RD));
     const int wm = warp % 2, wn = warp / 2;
     const int g = lane >> 2, tig = lane & 3;
-    const double* a_base = dA + wm * 64 + g + tig * DD_BM;
-    const double* b_base = dB + wn * 32 + g + tig * DD_BN;
+    const double* a_base = dA + wm * 64 + g + tig * DD_P;
+    const double* b_base = dB + wn * 32 + g + tig * DD_P;
     const uint32_t full_u = smem_u32(dfull), empty_u = smem_u32(dempty);
-    // ring position as (stage, phase) counters: no division by the 3-stage
-    // ring in the k loop of the group that bounds the pairing
-    int st = 0;
-    uint32_t ph = 0;
+    const uint32_t a_u = smem_u32(a_base), b_u = smem_u32(b_base);
+    // Ring position in one register: stage in bits 0-1, phase in bit 2; the
+    // k-block count runs down.  The loop state the D group keeps live at its
+    // register cap is the accumulators, the fragments, this word, the count
+    // and two shared addresses (the tile index waits in shared memory).
+    uint32_t ring = 0;
     for (;;) {
       // the producer names the next tile in its first stage's slot
-      mbar_wait_u32(full_u + 8 * st, ph);
-      int v = *reinterpret_cast<volatile int*>(&dslot[st]);
-      if (v < 0) break;
-      // only v stays live through the mainloop (the group runs at its register
-      // cap); the job and tile coordinates are derived again for the epilogue
-      const int nk = static_cast<int>(d.d[job_of(d.d, d.nd, v)].lpad / DU_BK);
+      mbar_wait_u32(full_u + 8 * (ring & 3), ring >> 2);
+      const int w0 = *reinterpret_cast<volatile int*>(&dslot[ring & 3]);
+      if (w0 < 0) break;
+      if (lane == 0) dtile[warp] = w0 >> 1;  // read back for the epilogue
       double acc[8][4][2];
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = st;
-        if (kb > 0) mbar_wait_u32(full_u + 8 * s, ph);
-        const double* a = a_base + s * DD_SA;
-        const double* b = b_base + s * DD_SB;
+      bool first = true, last;
+      do {
+        const uint32_t s = ring & 3;
+        if (!first) mbar_wait_u32(full_u + 8 * s, ring >> 2);
+        first = false;
+        last = *reinterpret_cast<volatile int*>(&dslot[s]) & 1;  // the producer marks the tile's last k-block
+        const uint32_t a = a_u + s * (DD_SA * 8), b = b_u + s * (DD_SB * 8);
 #pragma unroll
         for (int kk = 0; kk < DU_BK; kk += 4) {
           double af[8], bf[4];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) af[i] = a[kk * DD_BM + i * 8];
+          for (int j = 0; j < 4; ++j) bf[j] = lds_f64(b + (kk * DD_P + j * 8) * 8);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bf[j] = b[kk * DD_BN + j * 8];
+          for (int i = 0; i < 8; ++i) af[i] = lds_f64(a + (kk * DD_P + i * 8) * 8);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -401,18 +438,16 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         }
         fence_proxy_async();  // generic reads of the stage before its TMA refill
         __syncwarp();
-        if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
-        if (++st == DD_STAGES) {
-          st = 0;
-          ph ^= 1;
-        }
-      }
-      asm volatile("" : "+r"(v));
-      const int jx = job_of(d.d, d.nd, v);
+        if (lane0()) mbar_arrive_u32(empty_u + 8 * s);
+        ring = s + 1 == DD_STAGES ? (ring & 4) ^ 4 : ring + 1;
+      } while (!last);
+      __syncwarp();
+      const int vt = *reinterpret_cast<volatile int*>(&dtile[warp]);
+      const int jx = job_of(d.d, d.nd, vt);
       const DualJob* jp = &d.d[jx];
       int tm, tn;
-      tile_coords(jp->tile_begin + v - jp->tile0, jp->tiles_m, jp->tiles_n, 0, tm, tn);
-      MDG_DISPATCH_CDT(jp->out.dtype, CDT, { epilogue_d<CDT>(*jp, tm, tn, wm, wn, lane, acc); });
+      tile_coords(jp->tile_begin + vt - jp->tile0, jp->tiles_m, jp->tiles_n, 0, tm, tn);
+      MDG_DISPATCH_CDT(jp->out.dtype, CDT, { epilogue_d<CDT>(*jp, tm, tn, warp % 2, warp / 2, lane, acc); });
     }
     if (d.timing && lane == 0) atomicMax(&d.timing[1], globaltimer());
     return;
@@ -425,23 +460,25 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
   const float* a_base = fA + ty * 4;
   const float* b_base = fB + tx * 4;
   const uint32_t full_u = smem_u32(ffull), empty_u = smem_u32(fempty);
-  int it = 0;
+  int* ftile = dtile + DD_WARPS;  // F warps: the tile of the running mainloop
+  const int fw = warp - DD_WARPS;
+  uint32_t ring = 0;  // stage in bits 0-2, phase in bit 3
   for (;;) {
-    {
-      const int s0 = it % DF_STAGES;
-      mbar_wait_u32(full_u + 8 * s0, (it / DF_STAGES) & 1);
-    }
-    int v = *reinterpret_cast<volatile int*>(&fslot[it % DF_STAGES]);
-    if (v < 0) break;
-    const int nk = static_cast<int>(d.f[job_of(d.f, d.nf, v)].lpad / DF_BK);
+    mbar_wait_u32(full_u + 8 * (ring & 7), ring >> 3);
+    const int w0 = *reinterpret_cast<volatile int*>(&fslot[ring & 7]);
+    if (w0 < 0) break;
+    if (lane0()) ftile[fw] = w0 >> 1;  // read back for the epilogue
     uint64_t acc[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
-    for (int kb = 0; kb < nk; ++kb, ++it) {
-      const int s = it % DF_STAGES;
-      if (kb > 0) mbar_wait_u32(full_u + 8 * s, (it / DF_STAGES) & 1);
+    bool first = true, last;
+    do {
+      const uint32_t s = ring & 7;
+      if (!first) mbar_wait_u32(full_u + 8 * s, ring >> 3);
+      first = false;
+      last = *reinterpret_cast<volatile int*>(&fslot[s]) & 1;  // the producer marks the tile's last k-block
       const float* a = a_base + s * DF_SA;
       const float* b = b_base + s * DF_SB;
 #pragma unroll
@@ -462,9 +499,11 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
       }
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
-    }
-    asm volatile("" : "+r"(v));
+      if (lane0()) mbar_arrive_u32(empty_u + 8 * s);
+      ring = s + 1 == DF_STAGES ? (ring & 8) ^ 8 : ring + 1;
+    } while (!last);
+    __syncwarp();
+    const int v = *reinterpret_cast<volatile int*>(&ftile[fw]);
     const DualJob* jp = &d.f[job_of(d.f, d.nf, v)];
     int tm, tn;
     tile_coords(jp->tile_begin + v - jp->tile0, jp->tiles_m, jp->tiles_n, 0, tm, tn);
@@ -496,12 +535,11 @@ size_t dual_smem() { return DuRings<3, 4>::SMEM; }
 
 cudaError_t launch_gemm_dual(const DualDesc& d, int grid, cudaStream_t s) {
   if (grid <= 0 || (d.tiles_d == 0 && d.tiles_f == 0)) return cudaSuccess;
-  static const int variant = [] {  // tuning: MDGEMM_DUAL_STAGES = 0 (3 D / 4 F), 1 (3 / 5), 2 (4 / 4)
+  static const int variant = [] {  // tuning: MDGEMM_DUAL_STAGES = 0 (3 D / 4 F), 1 (3 / 5)
     const char* f = std::getenv("MDGEMM_DUAL_STAGES");
     return f ? std::atoi(f) : 0;
   }();
   if (variant == 1) return launch_stages<3, 5>(d, grid, s);
-  if (variant == 2) return launch_stages<4, 4>(d, grid, s);
   return launch_stages<3, 4>(d, grid, s);
 }
 

@@ -45,6 +45,27 @@ __global__ void fill_uniform_kernel(DView v, uint64_t state) {
   }
 }
 
+// normal(0,1) by Box-Muller over the same draws (the reference has no normal
+// generator; BASELINE configs[4] asks for normal entries): real component t
+// uses draws 2t and 2t+1 of the stream, u1 = (1 - d0) / 2 in (0, 1],
+// u2 = (1 + d1) / 2 in [0, 1), z = sqrt(-2 ln u1) cos(2 pi u2).
+__device__ __forceinline__ double normal_draw(uint64_t s, uint64_t t) {
+  const double u1 = 0.5 * (1.0 - uniform_draw(s, 2 * t));
+  const double u2 = 0.5 * (1.0 + uniform_draw(s, 2 * t + 1));
+  return sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+__global__ void fill_normal_kernel(DView v, uint64_t state) {
+  const int64_t total = v.m * v.n;
+  const bool cplx = dt_complex(v.dtype);
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % v.m, j = e / v.m;
+    const uint64_t t = static_cast<uint64_t>(j * v.m + i) * (cplx ? 2u : 1u);
+    st_elem(v, i, j, normal_draw(state, t), cplx ? normal_draw(state, t + 1) : 0.0);
+  }
+}
+
 int grid_for(int64_t total, int sms) {
   const int64_t blocks = (total + 255) / 256, cap = int64_t{sms > 0 ? sms : 1} * 32;
   return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
@@ -61,6 +82,12 @@ cudaError_t launch_beta_pass(const DView& out, const DBeta& beta, int sms, cudaS
 cudaError_t launch_fill_uniform(const DView& v, uint64_t state, int sms, cudaStream_t s) {
   if (v.m * v.n == 0) return cudaSuccess;
   fill_uniform_kernel<<<grid_for(v.m * v.n, sms), 256, 0, s>>>(v, state);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_normal(const DView& v, uint64_t state, int sms, cudaStream_t s) {
+  if (v.m * v.n == 0) return cudaSuccess;
+  fill_normal_kernel<<<grid_for(v.m * v.n, sms), 256, 0, s>>>(v, state);
   return cudaGetLastError();
 }
 

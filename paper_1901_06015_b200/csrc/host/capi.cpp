@@ -369,6 +369,16 @@ int mdg_fill_uniform(const mdg_view_t* v, uint64_t rng_state, void* stream) {
   });
 }
 
+int mdg_fill_normal(const mdg_view_t* v, uint64_t rng_state, void* stream) {
+  return guarded([&] {
+    const MatrixView mv = view_from(v);
+    prof::Scope scope(MDG_KERNEL_FILL, static_cast<cudaStream_t>(stream),
+                      static_cast<double>(mv.m) * mv.n * dtype_size(mv.dtype));
+    cuda_check(mdg::launch_fill_normal(to_dview(mv), rng_state, device_sms(), static_cast<cudaStream_t>(stream)),
+               "fill_normal");
+  });
+}
+
 uint64_t mdg_rng_split_tag(uint64_t state, const char* tag) {
   uint64_t h = state ^ kGamma;
   for (const char* p = tag; p && *p; ++p) h = splitmix(h ^ static_cast<uint64_t>(static_cast<unsigned char>(*p)));

@@ -143,6 +143,21 @@ def config(pairs: dict | None = None) -> M.Config:
     return c
 
 
+EPS = {M.SINGLE: 2.0 ** -24, M.DOUBLE: 2.0 ** -53}
+
+
+def frob_bound(label: str, k: int) -> float:
+    """North-star C bound (BASELINE.json): relative Frobenius error <= 4 k eps of
+    the computation precision; + eps of C's storage precision when that is
+    narrower (a reordered sum legitimately flips some of its roundings,
+    SURVEY 8(d))."""
+    dc, _, _, comp = label_dtypes(label)
+    bound = 4 * k * EPS[comp]
+    if M.precision_of(dc) != comp:
+        bound += EPS[M.precision_of(dc)]
+    return bound
+
+
 def rel_frobenius(got: np.ndarray, want: np.ndarray) -> float:
     g = got.astype(np.complex128)
     w = want.astype(np.complex128)

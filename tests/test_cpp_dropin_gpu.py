@@ -11,7 +11,7 @@ import pytest
 
 import paper_1901_06015_b200 as M
 from oracle import oracle as O
-from tests.helpers import Problem, SCALARS
+from tests.helpers import Problem, SCALARS, frob_bound, rel_frobenius
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -50,6 +50,7 @@ def test_cpp_drop_in(label, tmp_path):
     _, _, vc = p.views()
     _, _, va_after = p.views(C=after)
     assert O.orc_violation(alpha, va, vb, beta, vc, va_after, p.comp) <= 1.0
+    assert rel_frobenius(after.values(), want.values()) <= frob_bound(label, p.k)
     if cid not in (0, 7):
         r, _ = run(p, SCALARS["c55"], beta, "fast", tmp_path)
         assert r.returncode == 3 and "ScalarPolicyError" in r.stdout

@@ -12,19 +12,10 @@ import pytest
 
 import paper_1901_06015_b200 as M
 from oracle import oracle as O
-from tests.helpers import ALL_LABELS, HostMatrix, Problem, SCALARS, config, label_dtypes, rel_frobenius
+from tests.helpers import (ALL_LABELS, HostMatrix, Problem, SCALARS, config, frob_bound, label_dtypes,
+                           rel_frobenius)
 
 pytestmark = pytest.mark.gpu
-
-EPS = {M.SINGLE: 2.0 ** -24, M.DOUBLE: 2.0 ** -53}
-
-
-def frob_bound(label: str, k: int) -> float:
-    dc, _, _, comp = label_dtypes(label)
-    bound = 4 * k * EPS[comp]
-    if M.precision_of(dc) != comp:
-        bound += EPS[M.precision_of(dc)]
-    return bound
 
 
 def run_fast(p: Problem, alpha, beta, kv=None):

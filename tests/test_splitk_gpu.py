@@ -7,7 +7,7 @@ import pytest
 
 import paper_1901_06015_b200 as M
 from oracle import oracle as O
-from tests.helpers import Problem, SCALARS, config
+from tests.helpers import Problem, SCALARS, config, frob_bound, rel_frobenius
 
 pytestmark = pytest.mark.gpu
 
@@ -33,3 +33,21 @@ def test_splitk(label, splits, monkeypatch):
     va, vb, vc = p.views()
     _, _, va_after = p.views(C=after)
     assert O.orc_violation(alpha, va, vb, SCALARS["cfg2_beta"], vc, va_after, p.comp) <= 1.0
+    want = p.C.clone()
+    _, _, vw = p.views(C=want)
+    O.orc_gemm(alpha, va, vb, SCALARS["cfg2_beta"], vw)
+    assert rel_frobenius(after.values(), want.values()) <= frob_bound(label, p.k)
+
+
+def test_splitk_off_is_bitwise_the_unsplit_grid(monkeypatch):
+    # gpu.splitk = off: the same call as the whole-k grid, bit for bit, on a shape where auto splits
+    p = Problem("dddd", 70, 90, 2100, seed=5)
+    dA, dB, dC = p.device()
+    da, db, dc = p.views(A=dA, B=dB, C=dC)
+    M.gemm(SCALARS["p7"], da, db, SCALARS["m3"], dc, config({"gpu.numerics": "fast", "gpu.splitk": "off"}))
+    off = dC.bytes()
+    monkeypatch.setenv("MDGEMM_SPLITK", "1")  # forced factor 1 = the unsplit grid
+    dA, dB, dC = p.device()
+    da, db, dc = p.views(A=dA, B=dB, C=dC)
+    M.gemm(SCALARS["p7"], da, db, SCALARS["m3"], dc, config({"gpu.numerics": "fast"}))
+    assert np.array_equal(off, dC.bytes())
