@@ -76,12 +76,16 @@ def parse_args():
 
 
 # ------------------------------------------------------------------ workloads
-def workload(args):
-    """(description, [(label, m, n, k, alpha, beta)], distribution)."""
-    import paper_1901_06015_b200 as M
-    S = M.Scalar
+def workload(args, S=None):
+    """(description, [(label, m, n, k, alpha, beta)], distribution).  S: the Scalar struct class the
+    items are built with (the product's by default; the reference arm passes oracle.abi.Scalar so that
+    it never loads the product library)."""
+    from oracle import abi as A
+    if S is None:
+        import paper_1901_06015_b200 as M
+        S = M.Scalar
     if args.workload == "sweep":
-        labels = [l.str() for l in M.CaseLabel.all()]
+        labels = A.all_labels()
         if args.labels:
             labels = [l for l in args.labels.split(",") if l]
         if args.size:
@@ -92,7 +96,7 @@ def workload(args):
         items = []
         for s in sizes:
             for lab in labels:
-                cid = M.CaseLabel.parse(lab).case_id()
+                cid = A.case_id(lab)
                 alpha = S.complex_value(1.2, -0.7) if cid in (0, 7) else S.real_value(1.2)
                 items.append((lab, s, s, s, alpha, S.complex_value(0.9, 0.3)))
         span = f"m=n=k={sizes[0]}" if len(sizes) == 1 else f"m=n=k={sizes[0]}..{sizes[-1]} step {sizes[1] - sizes[0]}"
@@ -115,8 +119,8 @@ def workload(args):
 
 
 def useful_flops(items):
-    import paper_1901_06015_b200 as M
-    return sum(M.flops_of_case(M.CaseLabel.parse(l).case_id(), m, n, k) for l, m, n, k, _, _ in items)
+    from oracle import abi as A
+    return sum(A.flops_of_case(A.case_id(l), m, n, k) for l, m, n, k, _, _ in items)
 
 
 # ------------------------------------------------------------------ operands
@@ -496,6 +500,14 @@ def run_b200(args):
                       "step): each distinct host operand crosses PCIe once per step, each host C returns once",
                "timer": "host wall clock around synchronous calls"}
 
+    # ---- the reference arm's own sample (same labels, sizes, scalars): device-resident as one batch,
+    # and end to end through the unchanged per-call gemm() on pageable host buffers (one operand set
+    # per label, every call stages its own A, B, C in and C out) -- a like-for-like pair for the
+    # reference arm's number
+    same = None
+    if not args.no_e2e and world == 1:
+        same = same_config_run(M, args, stream)
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -530,6 +542,8 @@ def run_b200(args):
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,
+        "same_config_as_reference": same,
+        "libraries_loaded": loaded_libraries(),
     }
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = cpu_baseline(args)
@@ -538,10 +552,73 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def same_config_run(M, args, stream):
+    """The reference arm's sample on this GPU: device-resident (one gemm_batch, CUDA events) and
+    per-call gemm() from pageable host memory (host wall clock, every call synchronous)."""
+    import numpy as np
+    import torch
+    _, sample, text, dist_kind = reference_sample(args, M.Scalar)
+    flops = useful_flops(sample)
+    cfg = M.Config.defaults().set("gpu.numerics", args.numerics)
+    dev_ops, host_ops = [], []
+    for i, (l, m, n, k, al, be) in enumerate(sample):
+        dc, da, db = (M.dtype_from_letter(ch) for ch in l[:3])
+        comp = M.SINGLE if l[3] == "s" else M.DOUBLE
+        trip = []
+        for role, dt, (r, c) in (("a", da, (m, k)), ("b", db, (k, n)), ("c", dc, (m, n))):
+            t = torch.empty(max(r * c, 1) * M.dtype_size(dt), dtype=torch.uint8, device="cuda")
+            v = M.MatrixView.make(t.data_ptr(), r, c, 1, max(r, 1), dt)
+            state = M.Rng(args.seed).split(f"same/{l}/{role}").state
+            (M.fill_normal if dist_kind == "normal" else M.fill_uniform)(v, state, stream)
+            trip.append((t, v))
+        dev_ops.append((al, trip[0][1], trip[1][1], be, trip[2][1].with_comp_prec(comp)))
+        hs = []
+        for t, v in trip:
+            h = np.empty(t.numel(), np.uint8)  # pageable, like the reference's Matrix storage
+            h[:] = t.cpu().numpy()
+            hv = M.MatrixView.from_buffer_copy(v)
+            hv.base = h.ctypes.data
+            hs.append((h, hv))
+        host_ops.append((al, hs[0][1], hs[1][1], be, hs[2][1].with_comp_prec(comp), hs))
+    torch.cuda.synchronize()
+    M.gemm_batch(dev_ops, cfg, stream=stream, sync=False)  # warm-up
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        M.gemm_batch(dev_ops, cfg, stream=stream, sync=False)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    device = flops * len(times) / sum(times) / 1e9
+    for al, a, b, be, c, _ in host_ops:  # warm-up pass through the public per-call API
+        M.gemm(al, a, b, be, c, cfg)
+    s0 = M.staging_bytes()
+    gc.collect()
+    gc.disable()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for al, a, b, be, c, _ in host_ops:
+            M.gemm(al, a, b, be, c, cfg)
+    el = time.perf_counter() - t0
+    gc.enable()
+    s1 = M.staging_bytes()
+    return {"workload": text, "calls": len(sample), "flops_per_step": flops,
+            "device_resident": {"value": device, "unit": "GFLOPS", "api": "gemm_batch on device views, CUDA events"},
+            "e2e_per_call": {"value": flops * args.steps / el / 1e9, "unit": "GFLOPS",
+                             "h2d_bytes_per_step": (s1[0] - s0[0]) // args.steps,
+                             "d2h_bytes_per_step": (s1[1] - s0[1]) // args.steps,
+                             "api": "mdgemm::gemm / mdg_gemm per call on pageable host MatrixViews (synchronous, "
+                                    "one operand set per label; each call stages its operands in and C out)",
+                             "timer": "host wall clock"}}
+
+
 # ----------------------------------------------------------- reference arm
-def reference_sample(args):
-    import paper_1901_06015_b200 as M
-    desc, items, _ = workload(args)
+def reference_sample(args, S=None):
+    """The bounded CPU sample of the workload: every sweep label at m=n=k=--cpu-size (512), or a
+    512 x 512 column/row sub-block of a single-problem config with its full inner dimension."""
+    desc, items, dist_kind = workload(args, S)
     if args.workload == "sweep":
         s = args.cpu_size
         seen, sample = set(), []
@@ -556,39 +633,58 @@ def reference_sample(args):
             mm, nn = min(m, 512), min(n, 512)
             sample.append((l, mm, nn, k, al, be))
             text = f"{l} sub-block {mm}x{nn} with the full k={k}"
-    return desc, sample, text
+    return desc, sample, text, dist_kind
+
+
+def sample_operands(A, sample, seed, dist_kind, fill):
+    """Host operands of the CPU sample, one A/B/C per label and shape: uniform entries from the
+    reference Rng (the C restatement, bitwise the reference's fill_uniform), or normal(0,1) by the
+    same Box-Muller definition the device generator uses.  `fill(view, state)` fills a view."""
+    from oracle import oracle as O
+    mats, calls = {}, []
+    for l, m, n, k, al, be in sample:
+        dc, da, db = (A.dtype_from_letter(ch) for ch in l[:3])
+        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, n)), ("c", dc, (m, n))):
+            key = (l, role, shape)
+            if key not in mats:
+                h = A.HostMatrix(dt, *shape)
+                state = O.orc_rng_state(seed, [l, role, *shape])
+                if dist_kind == "normal":
+                    import numpy as np
+                    real = np.float32 if dt in (A.DT_S, A.DT_C) else np.float64
+                    h.buf.view(real)[:] = O.normal_values(state, np.arange(h.buf.size // np.dtype(real).itemsize))
+                else:
+                    fill(h.view(), state)
+                mats[key] = h
+        comp = A.SINGLE if l[3] == "s" else A.DOUBLE
+        calls.append((al, mats[(l, "a", (m, k))], mats[(l, "b", (k, n))], be, mats[(l, "c", (m, n))], comp))
+    return mats, calls
 
 
 def run_reference_steps(args, steps, warmup):
-    """Times the reference engine (oracle/_ref, built from the reference sources) through its
-    public gemm() on host memory, all host threads, ctemp=on."""
-    import paper_1901_06015_b200 as M
+    """Times the reference engine (oracle/_ref, built from the reference's own sources) through its
+    public gemm() on host memory, all host threads, ctemp=on.  Loads only oracle/ libraries: the
+    product package is never imported on this path."""
+    from oracle import abi as A
     from oracle import oracle as O
-    from tests.helpers import HostMatrix
 
     if O.ref is None:
         raise RuntimeError("oracle/_ref/libmdgemm_ref.so is missing")
     cores = os.cpu_count() or 1
-    cfg = M.Config.defaults().set("gemm.threads", cores).set("ctemp.enable", "on")
-    desc, sample, text = reference_sample(args)
-    mats = {}
-    calls = []
-    for l, m, n, k, al, be in sample:
-        dc, da, db = (M.dtype_from_letter(ch) for ch in l[:3])
-        for role, dt, shape in (("a", da, (m, k)), ("b", db, (k, n)), ("c", dc, (m, n))):
-            if (role, dt, shape) not in mats:
-                mats[(role, dt, shape)] = HostMatrix(dt, *shape).fill(O.orc_rng_state(args.seed, [role, dt, *shape]))
-        comp = M.SINGLE if l[3] == "s" else M.DOUBLE
-        calls.append((al, mats[("a", da, (m, k))].view(), mats[("b", db, (k, n))].view(), be,
-                      mats[("c", dc, (m, n))].view(comp=comp)))
+    cfg = O.ref_config_defaults()
+    cfg.threads = cores
+    cfg.ctemp = A.CTEMP_ON
+    desc, sample, text, dist_kind = reference_sample(args, A.Scalar)
+    _, calls = sample_operands(A, sample, args.seed, dist_kind, O.orc_fill_uniform)
+    views = [(al, a.view(), b.view(), be, c.view(comp=comp)) for al, a, b, be, c, comp in calls]
     flops = useful_flops(sample)
     for _ in range(warmup):
-        for c in calls:
+        for c in views:
             O.ref_gemm(*c, cfg)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        for c in calls:
+        for c in views:
             O.ref_gemm(*c, cfg)
         times.append(time.perf_counter() - t0)
     return desc, text, flops, times, cores
@@ -616,12 +712,27 @@ def run_reference(args):
         "n_gpus": int(os.environ.get("WORLD_SIZE", str(args.gpus))), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64/f32 (per label computation precision)", "data": "synthetic: reference Rng uniform[-1,1)",
-        "config": {"workload": desc, "numerics": "reference CPU engine"},
+        "config": {"workload": desc, "sample": text, "numerics": "reference CPU engine"},
         "cpu_baseline": {"value": value, "unit": "GFLOPS", "cores": cores, "kind": "reference",
                          "sample": f"{text}; reference gemm() with gemm.threads={cores}, ctemp.enable=on"},
         "e2e": {"value": value, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "libraries_loaded": loaded_libraries(),
     }
     print(json.dumps(line), flush=True)
+
+
+def loaded_libraries():
+    """The repo's shared objects mapped into this process (evidence of which code ran)."""
+    out = []
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if len(line.split()) >= 6 else ""
+            rel = os.path.relpath(path, ROOT) if path.startswith(ROOT) and path.endswith(".so") else None
+            if rel and rel not in out:
+                out.append(rel)
+    except OSError:
+        pass
+    return out
 
 
 def main():

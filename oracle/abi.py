@@ -56,6 +56,11 @@ def case_id(label: str) -> int:
     return 3 if not a and not b else 5 if a else 6
 
 
+def all_labels() -> list[str]:
+    """CaseLabel::all() (case_label.cpp:28-39): C, A, B over s d c z, then s d."""
+    return [c + a + b + p for c in _LETTERS for a in _LETTERS for b in _LETTERS for p in "sd"]
+
+
 def flops_of_case(cid: int, m: int, n: int, k: int) -> int:
     """dispatch.cpp:35-54: 2mnk (0, 1a, 1b, 1c), 4mnk (2ab, 2ac, 2bc), 8mnk (3)."""
     return (2 if cid <= 3 else 4 if cid <= 6 else 8) * m * n * k
@@ -137,3 +142,19 @@ def convert(T, obj):
     if ctypes.sizeof(obj) != ctypes.sizeof(T):
         raise TypeError(f"{type(obj).__name__} does not have the layout of {T.__name__}")
     return T.from_buffer_copy(obj)
+
+
+class HostMatrix:
+    """A column-major host matrix (numpy buffer) and its view, for the CPU
+    checkers and the reference arm (Matrix::make, matrix.hpp:17-43)."""
+
+    def __init__(self, dtype: int, m: int, n: int):
+        import numpy as np
+        self.dtype, self.m, self.n = dtype, m, n
+        self.buf = np.zeros(max(m * n, 1) * dtype_size(dtype), np.uint8)
+
+    def view(self, comp: int | None = None) -> MatrixView:
+        v = MatrixView(self.buf.ctypes.data, self.m, self.n, 1, max(self.m, 1), self.dtype, 0,
+                       (SINGLE if self.dtype in (DT_S, DT_C) else DOUBLE) if comp is None else comp,
+                       self.dtype)
+        return v

@@ -102,6 +102,12 @@ def _args(alpha, a, b, beta, c, cfg):
             convert(MatrixView, c), convert(Config, cfg))
 
 
+def ref_config_defaults() -> Config:
+    out = Config()
+    check_ref(ref.ref_config_defaults(byref(out)))
+    return out
+
+
 def orc_config_defaults() -> Config:
     out = Config()
     check_orc(orc.orc_config_defaults(byref(out)))

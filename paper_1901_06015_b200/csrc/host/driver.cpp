@@ -130,6 +130,51 @@ double pack_traffic(const MatrixView& src, size_t packed) {
   return static_cast<double>(src.m) * src.n * dtype_size(src.dtype) + static_cast<double>(packed);
 }
 
+// Real inner-dimension steps per source column of A (left) / row of B (right):
+// 2 for the 1m formats (1e, 1r), 1 for Standard.
+int64_t k_factor(PackFormat f) { return f == PackFormat::Standard ? 1 : 2; }
+
+// The plan restricted to real inner steps [lo, hi): column slices of A's
+// source view, row slices of B's.
+ExecutionPlan k_slice(const ExecutionPlan& p, int64_t lo, int64_t hi, int64_t f_a, int64_t f_b) {
+  ExecutionPlan q = p;
+  q.k = hi - lo;
+  q.a.base = p.a.base + static_cast<size_t>(lo / f_a * p.a.cs) * dtype_size(p.a.dtype);
+  q.a.n = (hi - lo) / f_a;
+  q.b.base = p.b.base + static_cast<size_t>(lo / f_b * p.b.rs) * dtype_size(p.b.dtype);
+  q.b.m = (hi - lo) / f_b;
+  return q;
+}
+
+bool onem_direct(const ExecutionPlan& p);
+
+}  // namespace
+
+// FAST per-KC-block structure of a plan without C_temp: 0 none (one combine
+// after the full inner dimension is exact for C_temp plans and the Direct
+// paths: they accumulate continuously in the computation precision), 1 one
+// combine per KC block (Temp path), 2 the first KC block then the rest (1m
+// with a complex beta).  Odd KC blocks of a 1m image would split a complex
+// element's real and imaginary steps; those plans keep one combine.
+int fast_block_mode(const ExecutionPlan& p, int64_t* f_a, int64_t* f_b) {
+  if (p.ctemp || p.k <= p.params.kc || p.params.kc < 1) return 0;
+  const int64_t fa = k_factor(p.format_a), fb = k_factor(p.format_b);
+  if (p.params.kc % fa || p.params.kc % fb) return 0;
+  int mode = 0;
+  const bool onem = p.ukr_path == UkrPath::OneMColumn || p.ukr_path == UkrPath::OneMRow;
+  if (p.ukr_path == UkrPath::Temp) mode = 1;
+  if (onem && !onem_direct(p)) {
+    const FlattenAxis ax = p.ukr_path == UkrPath::OneMColumn ? FlattenAxis::Rows : FlattenAxis::Cols;
+    const bool flat = p.c.dtype.precision == p.comp_prec && can_flatten(p.c, ax);
+    mode = flat ? 2 : 1;  // complex beta on a flattenable C: virtual_ukr_onem's mixed route
+  }
+  if (f_a) *f_a = fa;
+  if (f_b) *f_b = fb;
+  return mode;
+}
+
+namespace {
+
 bool onem_direct(const ExecutionPlan& p) {
   const FlattenAxis ax = p.ukr_path == UkrPath::OneMColumn ? FlattenAxis::Rows : FlattenAxis::Cols;
   return p.beta.im == 0.0 && p.c.dtype.precision == p.comp_prec && can_flatten(p.c, ax);
@@ -353,7 +398,7 @@ size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, b
 }
 
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared,
-                       void* arena, size_t arena_bytes, size_t* ws_needed, bool allow_splitk) {
+                       void* arena, size_t arena_bytes, size_t* ws_needed, bool allow_splitk, bool block_split) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (ws_needed) *ws_needed = 0;
   if (p.m == 0 || p.n == 0) return;
@@ -386,6 +431,34 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   const bool single = p.comp_prec == Precision::Single;
   const bool exact = numerics == Numerics::Exact;
   const int sms = device_sms();
+
+  // ctemp.enable = off (or auto with several threads) on a Temp-path plan: the
+  // reference rounds each KC block's partial sum into C (gemm_core.cpp:125-127,
+  // kernels.cpp:97-132).  FAST keeps that structure: one kernel pass per KC
+  // block of the real inner dimension, beta on the first and 1 afterwards
+  // (1m with a complex beta: the first block, then the rest in one pass,
+  // kernels.cpp:141-150).
+  if (!exact && block_split) {
+    int64_t f_a = 1, f_b = 1;
+    const int mode = fast_block_mode(p, &f_a, &f_b);
+    if (mode != 0) {
+      const int64_t kc = p.params.kc;
+      if (ws_needed) {  // the first (largest) block's workspace
+        ExecutionPlan q = k_slice(p, 0, std::min(kc, p.k), f_a, f_b);
+        execute_scheduled(q, numerics, nullptr, nullptr, shared, nullptr, 0, ws_needed, allow_splitk, false);
+        return;
+      }
+      for (int64_t pc = 0; pc < p.k;) {
+        const int64_t hi = mode == 2 && pc > 0 ? p.k : std::min(pc + kc, p.k);
+        ExecutionPlan q = k_slice(p, pc, hi, f_a, f_b);
+        if (pc > 0) q.beta = Scalar{1.0, 0.0, p.beta.dtype};
+        execute_scheduled(q, numerics, stream_ptr, nullptr, shared, arena, arena_bytes, nullptr, allow_splitk, false);
+        pc = hi;
+      }
+      if (fc) fc->add(reference_flops(p));
+      return;
+    }
+  }
 
   mdg::FastTile tile{64, 64, 1};
   if (!exact) tile = single ? mdg::choose_ffma_tile(p.m, p.n, sms) : mdg::choose_dmma_tile(p.m, p.n, sms);
@@ -619,6 +692,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
 // ---------------------------------------------------------------- dual-pipe jobs
 bool dual_eligible(const ExecutionPlan& p, Numerics numerics) {
   if (numerics != Numerics::Fast || p.m <= 0 || p.n <= 0 || p.k <= 0) return false;
+  if (fast_block_mode(p) != 0) return false;  // per-KC-block rounding into C: execute()
   if (p.c.dtype.domain == Domain::Complex && p.pair_axis == PairAxis::None) return false;
   const int64_t bm = p.comp_prec == Precision::Single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
   const int64_t tiles = ((p.m + bm - 1) / bm) * ((p.n + mdg::DUAL_D_BN - 1) / mdg::DUAL_D_BN);

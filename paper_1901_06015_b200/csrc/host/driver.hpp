@@ -63,7 +63,7 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
 // would use, launching nothing.
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared,
                        void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr,
-                       bool allow_splitk = true);
+                       bool allow_splitk = true, bool block_split = true);
 size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, bool allow_splitk = true);
 
 // ---- the dual-pipe kernel (gemm_dual.cu), used by gemm_batch -------------
@@ -97,6 +97,11 @@ struct DualPiece {
 };
 std::vector<DualPiece> dual_schedule_pieces(const std::vector<GemmCall>& calls, const Config& cfg,
                                             std::vector<int32_t>* call_tiles);
+
+// FAST numerics of a plan without C_temp whose Temp / 1m route rounds into C
+// per KC block: 0 none, 1 per KC block, 2 first block then the rest (see
+// driver.cpp); f_a / f_b receive the real inner steps per source column / row.
+int fast_block_mode(const ExecutionPlan& p, int64_t* f_a = nullptr, int64_t* f_b = nullptr);
 
 // The value the reference's FlopCounter reaches for this plan.
 uint64_t reference_flops(const ExecutionPlan& p);

@@ -50,6 +50,9 @@ def test_oracle_abi_mirror_matches_the_product_layout():
                 label = "dz"[c] + "dz"[a] + "dz"[b] + "d"
                 assert A.case_id(label) == M.classify_case(bool(c), bool(a), bool(b))
     assert A.flops_of_case(7, 3, 5, 7) == M.flops_of_case(7, 3, 5, 7)
+    assert A.all_labels() == [l.str() for l in M.CaseLabel.all()]
+    h = A.HostMatrix(M.DT_C, 5, 3)
+    assert bytes(h.view()) == bytes(M.MatrixView.make(h.buf.ctypes.data, 5, 3, 1, 5, M.DT_C))
 
 
 def test_config_keys_and_errors():
