@@ -13,6 +13,7 @@
 
 #include <complex>
 #include <cstddef>
+#include <memory>
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
@@ -306,6 +307,52 @@ void gemm_async(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar b
 // dispatch.cpp:359-388 crosses).
 void execute(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc = nullptr,
              bool allow_splitk = true);
+
+// ------------------------------------------------------------ multi-GPU
+// C and B split into column panels, A broadcast once over
+// NVLink / NVSwitch (NCCL, loaded at run time), no reduction.
+
+// Columns [*j0, *j0 + *nb) of n owned by `rank` of `world`: equal panels,
+// multiples of `align` columns, the last one shorter (or empty).
+void shard_columns(std::int64_t n, int world, int rank, std::int64_t align, std::int64_t* j0, std::int64_t* nb);
+
+// A communicator of one process per GPU (NCCL, on the current device).
+struct CommId {
+  unsigned char bytes[128];
+};
+class Communicator {
+ public:
+  static CommId unique_id();                          // on one rank; share it with the others
+  Communicator(const CommId& id, int nranks, int rank);  // collective over the ranks
+  ~Communicator();
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  int size() const;
+  int rank() const;
+  int device() const;
+  struct Impl;
+
+ private:
+  std::unique_ptr<Impl> impl_;
+  friend void gemm_sharded(Communicator&, int, Scalar, const MatrixView&, const MatrixView&, Scalar,
+                           const MatrixView&, const Config&, void*, FlopCounter*);
+};
+
+// This rank's column panel of C := beta*C + alpha*A*B: `a` is the root's A
+// (on other ranks the same geometry; base null = the library receives it),
+// b_panel / c_panel this rank's device column panels (shard_columns).  A
+// goes to every rank by broadcast while each rank packs its B panel.
+// Ordered on `stream` (a cudaStream_t), no host synchronisation.  A shard
+// never takes split-K.
+void gemm_sharded(Communicator& comm, int root, Scalar alpha, const MatrixView& a, const MatrixView& b_panel,
+                  Scalar beta, const MatrixView& c_panel, const Config& cfg = Config::defaults(),
+                  void* stream = nullptr, FlopCounter* fc = nullptr);
+
+// The whole call over several GPUs of this process: A, B, C anywhere (host
+// or device memory); column panels of B and C go to `devices`, A is
+// broadcast from the first one, C panels come back.  Synchronous.
+void gemm_multi(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
+                const Config& cfg, const std::vector<int>& devices, FlopCounter* fc = nullptr);
 
 // --------------------------------------------------------------- case labels
 struct CaseLabel {

@@ -238,6 +238,29 @@ uint64_t mdg_rng_split_salt(uint64_t state, uint64_t salt);
 int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align,
                       int64_t* j0, int64_t* nb);
 
+/* ---- multi-GPU: C and B column panels, A broadcast over
+ * NVLink / NVSwitch with NCCL (loaded at run time), no reduction ---------
+ * mdg_comm_*: one process per GPU.  Rank 0 gets an id (mdg_comm_unique_id),
+ * the caller shares the 128 bytes with the other ranks (any out-of-band
+ * channel), and every rank calls mdg_comm_init on its own device.
+ * mdg_gemm_sharded: this rank's panel of C := beta*C + alpha*A*B; `a` is A on
+ * the root (other ranks: the same geometry, base null = library-owned
+ * receive buffer); b_panel / c_panel are this rank's device panels
+ * (mdg_shard_columns).  Stream-ordered, no host synchronisation.
+ * mdg_gemm_multi: the whole call over `ndev` GPUs of this process
+ * (operands in host or device memory), synchronous. */
+typedef struct mdg_comm* mdg_comm_t;
+enum { MDG_COMM_ID_BYTES = 128 };
+int mdg_comm_unique_id(uint8_t* id /* [MDG_COMM_ID_BYTES] */);
+int mdg_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, mdg_comm_t* out);
+int mdg_comm_destroy(mdg_comm_t comm);
+int mdg_gemm_sharded(mdg_comm_t comm, int32_t root, mdg_scalar_t alpha, const mdg_view_t* a,
+                     const mdg_view_t* b_panel, mdg_scalar_t beta, const mdg_view_t* c_panel,
+                     const mdg_config_t* cfg, void* stream, uint64_t* flops_out);
+int mdg_gemm_multi(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b, mdg_scalar_t beta,
+                   const mdg_view_t* c, const mdg_config_t* cfg, int32_t ndev, const int32_t* devices,
+                   uint64_t* flops_out);
+
 /* ---- instrumentation (the reference's FlopCounter, extended per kernel) ---
  * Every kernel the library launches bumps a process-wide counter.  Between
  * mdg_profile_begin() and mdg_profile_end() the calling thread also brackets

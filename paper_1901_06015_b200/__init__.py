@@ -18,7 +18,7 @@ from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, 
 __all__ = [
     "Error", "ScalarPolicyError", "CudaError", "lib", "MatrixView", "Scalar", "Config", "ExecutionPlan",
     "plan", "gemm", "gemm_batch", "gemm_async", "execute", "pack_block_device", "packed_bytes", "fill_uniform", "fill_normal",
-    "Rng", "classify_case", "flops_of_case", "apply_scalar_policy", "shard_columns", "CaseLabel",
+    "Rng", "Comm", "comm_unique_id", "gemm_sharded", "gemm_multi", "classify_case", "flops_of_case", "apply_scalar_policy", "shard_columns", "CaseLabel",
     "DT_S", "DT_D", "DT_C", "DT_Z", "SINGLE", "DOUBLE", "LEFT", "RIGHT", "STANDARD", "ONE_E", "ONE_R",
     "FAST", "EXACT", "dtype_from_letter", "dtype_letter", "dtype_size", "is_complex", "precision_of",
     "CASE_NAMES",
@@ -262,6 +262,11 @@ def _load() -> ctypes.CDLL:
         "mdg_rng_split_salt": (c_uint64, [c_uint64, c_uint64]),
         "mdg_shard_columns": (c_int, [c_int64, c_int32, c_int32, c_int64, POINTER(c_int64), POINTER(c_int64)]),
         "mdg_trim_workspace": (c_int, [c_uint64]),
+        "mdg_comm_unique_id": (c_int, [ctypes.c_char_p]),
+        "mdg_comm_init": (c_int, [ctypes.c_char_p, c_int32, c_int32, POINTER(c_void_p)]),
+        "mdg_comm_destroy": (c_int, [c_void_p]),
+        "mdg_gemm_sharded": (c_int, [c_void_p, c_int32, S, V, V, S, V, C, c_void_p, POINTER(c_uint64)]),
+        "mdg_gemm_multi": (c_int, [S, V, V, S, V, C, c_int32, POINTER(c_int32), POINTER(c_uint64)]),
         "mdg_launch_count": (c_uint64, []),
         "mdg_staging_bytes": (None, [POINTER(c_uint64), POINTER(c_uint64)]),
         "mdg_profile_begin": (c_int, []),
@@ -281,6 +286,7 @@ EXPORTED_SYMBOLS = (
     "mdg_dual_schedule",
     "mdg_packed_bytes", "mdg_pack_operand",
     "mdg_fill_uniform", "mdg_fill_normal", "mdg_rng_split_tag", "mdg_rng_split_salt", "mdg_shard_columns",
+    "mdg_comm_unique_id", "mdg_comm_init", "mdg_comm_destroy", "mdg_gemm_sharded", "mdg_gemm_multi",
     "mdg_trim_workspace", "mdg_launch_count", "mdg_staging_bytes", "mdg_profile_begin", "mdg_profile_end",
 )
 
@@ -440,6 +446,61 @@ def shard_columns(n: int, world: int, rank: int, align: int = 1) -> tuple[int, i
     j0, nb = c_int64(0), c_int64(0)
     _check(lib.mdg_shard_columns(n, world, rank, align, byref(j0), byref(nb)))
     return j0.value, nb.value
+
+
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """A fresh communicator id (on one rank; share the bytes with the others)."""
+    buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+    _check(lib.mdg_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """One process per GPU: the library's NCCL communicator on the current device (mdg_comm_init).
+    Collective: every rank constructs it with the same id."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != COMM_ID_BYTES:
+            raise Error("Comm: the id must be 128 bytes")
+        self.handle = c_void_p()
+        _check(lib.mdg_comm_init(uid, nranks, rank, byref(self.handle)))
+        self.nranks, self.rank = nranks, rank
+
+    def close(self) -> None:
+        if self.handle:
+            _check(lib.mdg_comm_destroy(self.handle))
+            self.handle = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def gemm_sharded(comm: Comm, root: int, alpha: Scalar, a: MatrixView, b_panel: MatrixView, beta: Scalar,
+                 c_panel: MatrixView, cfg: Config | None = None, stream=None) -> int:
+    """This rank's column panel (mdg_gemm_sharded): A broadcast from `root` over the communicator
+    (a.base = 0 on other ranks: the library receives it), B / C panels on this rank's device."""
+    flops = c_uint64(0)
+    _check(lib.mdg_gemm_sharded(comm.handle, root, alpha, byref(a), byref(b_panel), beta, byref(c_panel),
+                                byref(cfg or Config.defaults()), _stream_ptr(stream), byref(flops)))
+    return flops.value
+
+
+def gemm_multi(alpha: Scalar, a: MatrixView, b: MatrixView, beta: Scalar, c: MatrixView, cfg: Config | None = None,
+               devices=None) -> int:
+    """The whole call over several GPUs of this process (mdg_gemm_multi), synchronous."""
+    import torch
+    devs = list(devices) if devices is not None else list(range(torch.cuda.device_count()))
+    arr = (c_int32 * len(devs))(*devs)
+    flops = c_uint64(0)
+    _check(lib.mdg_gemm_multi(alpha, byref(a), byref(b), beta, byref(c), byref(cfg or Config.defaults()), len(devs),
+                              arr, byref(flops)))
+    return flops.value
 
 
 class Rng:

@@ -389,12 +389,55 @@ uint64_t mdg_rng_split_salt(uint64_t state, uint64_t salt) { return splitmix(sta
 
 int mdg_shard_columns(int64_t n, int32_t world, int32_t rank, int64_t align, int64_t* j0, int64_t* nb) {
   return guarded([&] {
-    if (world < 1 || rank < 0 || rank >= world || n < 0 || align < 1) throw Error("mdg_shard_columns: bad arguments");
-    const int64_t per = (n + world - 1) / world;
-    const int64_t chunk = (per + align - 1) / align * align;
-    const int64_t lo = std::min<int64_t>(static_cast<int64_t>(rank) * chunk, n);
-    *j0 = lo;
-    *nb = std::min<int64_t>(chunk, n - lo);
+    if (!j0 || !nb) throw Error("mdg_shard_columns: bad arguments");
+    shard_columns(n, world, rank, align, j0, nb);
+  });
+}
+
+int mdg_comm_unique_id(uint8_t* id) {
+  return guarded([&] {
+    if (!id) throw Error("mdg_comm_unique_id: null id");
+    const CommId c = Communicator::unique_id();
+    std::memcpy(id, c.bytes, sizeof(c.bytes));
+  });
+}
+
+int mdg_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, mdg_comm_t* out) {
+  return guarded([&] {
+    if (!id || !out) throw Error("mdg_comm_init: bad arguments");
+    CommId c;
+    std::memcpy(c.bytes, id, sizeof(c.bytes));
+    *out = reinterpret_cast<mdg_comm_t>(new Communicator(c, nranks, rank));
+  });
+}
+
+int mdg_comm_destroy(mdg_comm_t comm) {
+  return guarded([&] { delete reinterpret_cast<Communicator*>(comm); });
+}
+
+int mdg_gemm_sharded(mdg_comm_t comm, int32_t root, mdg_scalar_t alpha, const mdg_view_t* a,
+                     const mdg_view_t* b_panel, mdg_scalar_t beta, const mdg_view_t* c_panel,
+                     const mdg_config_t* cfg, void* stream, uint64_t* flops_out) {
+  return guarded([&] {
+    if (!comm) throw Error("mdg_gemm_sharded: null communicator");
+    FlopCounter fc;
+    gemm_sharded(*reinterpret_cast<Communicator*>(comm), root, scalar_from(alpha), view_from(a), view_from(b_panel),
+                 scalar_from(beta), view_from(c_panel), config_from(cfg), stream, &fc);
+    if (flops_out) *flops_out = fc.value();
+  });
+}
+
+int mdg_gemm_multi(mdg_scalar_t alpha, const mdg_view_t* a, const mdg_view_t* b, mdg_scalar_t beta,
+                   const mdg_view_t* c, const mdg_config_t* cfg, int32_t ndev, const int32_t* devices,
+                   uint64_t* flops_out) {
+  return guarded([&] {
+    if (ndev < 1) throw Error("mdg_gemm_multi: ndev must be at least 1");
+    std::vector<int> devs(static_cast<size_t>(ndev));
+    for (int32_t i = 0; i < ndev; ++i) devs[i] = devices ? devices[i] : i;
+    FlopCounter fc;
+    gemm_multi(scalar_from(alpha), view_from(a), view_from(b), scalar_from(beta), view_from(c), config_from(cfg), devs,
+               &fc);
+    if (flops_out) *flops_out = fc.value();
   });
 }
 

@@ -398,7 +398,8 @@ size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, b
 }
 
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_ptr, FlopCounter* fc, bool shared,
-                       void* arena, size_t arena_bytes, size_t* ws_needed, bool allow_splitk, bool block_split) {
+                       void* arena, size_t arena_bytes, size_t* ws_needed, bool allow_splitk, bool block_split,
+                       const OperandReady* ready) {
   cudaStream_t st = static_cast<cudaStream_t>(stream_ptr);
   if (ws_needed) *ws_needed = 0;
   if (p.m == 0 || p.n == 0) return;
@@ -452,7 +453,8 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
         const int64_t hi = mode == 2 && pc > 0 ? p.k : std::min(pc + kc, p.k);
         ExecutionPlan q = k_slice(p, pc, hi, f_a, f_b);
         if (pc > 0) q.beta = Scalar{1.0, 0.0, p.beta.dtype};
-        execute_scheduled(q, numerics, stream_ptr, nullptr, shared, arena, arena_bytes, nullptr, allow_splitk, false);
+        execute_scheduled(q, numerics, stream_ptr, nullptr, shared, arena, arena_bytes, nullptr, allow_splitk, false,
+                          ready);
         pc = hi;
       }
       if (fc) fc->add(reference_flops(p));
@@ -571,7 +573,26 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   char* wsa = static_cast<char*>(ws);
   cudaError_t err = flag_bytes > 0 ? cudaMemsetAsync(wsa + off_f, 0, flag_bytes, st) : cudaSuccess;
   cuda_check(err, "stream-K flags");
-  if (mdg::pack_pair_ok(pa.desc, pb.desc)) {  // both operands in one launch
+  if (ready && ready->event) {
+    // one operand arrives on another stream (gemm_sharded: the broadcast of
+    // A): pack the other one first, then wait for it and pack it
+    const bool right_late = ready->right;
+    const Packed& first = right_late ? pa : pb;
+    const Packed& late = right_late ? pb : pa;
+    const MatrixView& fv = right_late ? p.a : p.b;
+    const MatrixView& lv = right_late ? p.b : p.a;
+    char* fdst = right_late ? wsa : wsa + off_b;
+    char* ldst = right_late ? wsa + off_b : wsa;
+    {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(fv, first.bytes));
+      err = mdg::launch_pack(first.desc, fdst, st);
+    }
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(st, ready->event, 0);
+    if (err == cudaSuccess) {
+      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(lv, late.bytes));
+      err = mdg::launch_pack(late.desc, ldst, st);
+    }
+  } else if (mdg::pack_pair_ok(pa.desc, pb.desc)) {  // both operands in one launch
     prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, pa.bytes) + pack_traffic(p.b, pb.bytes));
     err = mdg::launch_pack_pair(pa.desc, wsa, pb.desc, wsa + off_b, st);
   } else {

@@ -53,6 +53,15 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
                               Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
                               void* stream);
 
+// An operand of a call that becomes ready on another stream (gemm_sharded:
+// A arrives by broadcast): execute_scheduled packs the other operand first and
+// makes the stream wait on `event` before packing this one.  `right`: the
+// operand is the plan's right (B-side) operand (a transposed plan).
+struct OperandReady {
+  cudaEvent_t event = nullptr;
+  bool right = false;
+};
+
 // execute() with the scheduling hint of the batch runner: `shared` = other
 // calls of the same batch may run concurrently on the device, so the kernel
 // keeps the hardware-scheduled classic grid (whose waves interleave with the
@@ -63,7 +72,7 @@ void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackF
 // would use, launching nothing.
 void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream, FlopCounter* fc, bool shared,
                        void* arena = nullptr, size_t arena_bytes = 0, size_t* ws_needed = nullptr,
-                       bool allow_splitk = true, bool block_split = true);
+                       bool allow_splitk = true, bool block_split = true, const struct OperandReady* ready = nullptr);
 size_t workspace_bytes(const ExecutionPlan& p, Numerics numerics, bool shared, bool allow_splitk = true);
 
 // ---- the dual-pipe kernel (gemm_dual.cu), used by gemm_batch -------------
