@@ -16,6 +16,7 @@
 #include <memory>
 #include <cstdint>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -175,6 +176,64 @@ void pack_block_device(void* dst, const MatrixView& src, Side side, PackFormat f
                        Scalar scale, Datatype target, std::int64_t reg_block,
                        void* stream = nullptr);
 
+// The reference's pack seam (packing.hpp:27-130) on the device.  A packed
+// operand block: zero-padded register panels over one dimension, contiguous
+// along the other; the packed logical matrix is the operand after format
+// expansion.  The panels are produced by the sm_100a pack kernels (byte for
+// byte the reference's pack); `storage` may be host or device memory, the
+// source view too (host sources are staged through HBM).  Synchronous.
+class PackedBlock {
+ public:
+  PackedBlock() = default;
+  PackedBlock(const PackedBlock&) = delete;
+  PackedBlock& operator=(const PackedBlock&) = delete;
+  PackedBlock(PackedBlock&&) = default;
+  PackedBlock& operator=(PackedBlock&&) = default;
+
+  std::span<const std::byte> buf() const { return buf_; }
+  Datatype dtype() const { return dtype_; }
+  PackFormat format() const { return format_; }
+  Side side() const { return side_; }
+  // panel geometry in packed-logical units (complex elements for a
+  // Standard-packed complex operand, real elements otherwise)
+  std::int64_t panel_dim() const { return panel_dim_; }
+  std::int64_t panels() const { return panels_; }
+  std::int64_t panel_len() const { return panel_len_; }
+  std::int64_t logical_rows() const { return logical_rows_; }
+  std::int64_t logical_cols() const { return logical_cols_; }
+  std::int64_t padded_rows() const { return side_ == Side::Left ? panels_ * panel_dim_ : logical_rows_; }
+  std::int64_t padded_cols() const { return side_ == Side::Right ? panels_ * panel_dim_ : logical_cols_; }
+  // element (i, j) of the zero-padded packed logical matrix
+  std::complex<double> packed_element(std::int64_t i, std::int64_t j) const;
+  // as real register panels: a Standard-packed complex block doubles its panel dimension
+  std::int64_t kernel_panel_dim() const { return panel_dim_ * (dtype_.domain == Domain::Complex ? 2 : 1); }
+  std::int64_t kernel_panel_len() const { return panel_len_; }
+  Precision kernel_precision() const { return dtype_.precision; }
+  const std::byte* panel_ptr(std::int64_t p) const { return buf_.data() + static_cast<std::size_t>(p) * panel_bytes(); }
+  std::size_t panel_bytes() const { return static_cast<std::size_t>(panel_dim_ * panel_len_) * dtype_size(dtype_); }
+
+ private:
+  friend PackedBlock pack_block_panels(std::span<std::byte>, const MatrixView&, Side, PackFormat, bool, Scalar,
+                                       Datatype, std::int64_t, std::int64_t, std::int64_t);
+  friend PackedBlock pack_block(const MatrixView&, Side, PackFormat, bool, Scalar, Datatype, std::int64_t);
+  std::span<std::byte> buf_;
+  std::vector<std::byte> owned_;
+  Datatype dtype_ = dt_d;
+  PackFormat format_ = PackFormat::Standard;
+  Side side_ = Side::Left;
+  std::int64_t panel_dim_ = 0, panels_ = 0, panel_len_ = 0, logical_rows_ = 0, logical_cols_ = 0;
+};
+
+// packing.hpp:101-130: pack into a fresh host buffer / into caller storage /
+// only panels [panel_begin, panel_end) of it (other panels' bytes untouched).
+PackedBlock pack_block(const MatrixView& src, Side side, PackFormat format, bool conj, Scalar scale, Datatype target,
+                       std::int64_t reg_block);
+PackedBlock pack_block_into(std::span<std::byte> storage, const MatrixView& src, Side side, PackFormat format,
+                            bool conj, Scalar scale, Datatype target, std::int64_t reg_block);
+PackedBlock pack_block_panels(std::span<std::byte> storage, const MatrixView& src, Side side, PackFormat format,
+                              bool conj, Scalar scale, Datatype target, std::int64_t reg_block,
+                              std::int64_t panel_begin, std::int64_t panel_end);
+
 // ------------------------------------------------------------------- config
 struct BlockingParams {
   std::int64_t mc = 0;
@@ -189,6 +248,11 @@ enum class CTempMode : std::uint8_t { Auto, On, Off };
 
 // B200 extension: which device arithmetic gemm() uses (see mdgemm_b200.h).
 enum class Numerics : std::uint8_t { Fast, Exact };
+// The default of Config::numerics: FAST, or the environment's
+// MDGEMM_GPU_NUMERICS (fast | exact) -- so code that never touches the key
+// (the reference's own tests, built against this header) can run either
+// arithmetic.
+Numerics default_numerics();
 
 struct Config {
   BlockingParams single_params{128, 1024, 256, 8, 8, 1};
@@ -196,7 +260,7 @@ struct Config {
   int threads = 1;
   Preference preference = Preference::Column;
   CTempMode ctemp = CTempMode::Auto;
-  Numerics numerics = Numerics::Fast;
+  Numerics numerics = default_numerics();
   // B200 extension (gpu.splitk = auto | off): FAST calls whose tile grid
   // fills less than half of the GPU may split the inner dimension over
   // several CTAs (deterministic, but a different summation order than the

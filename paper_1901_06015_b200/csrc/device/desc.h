@@ -78,7 +78,8 @@ struct PackDesc {
   int64_t lpad;            // allocated panel length (>= len), zero-filled
   int64_t ext_i, ext_j;    // source index space incl. panel padding
   int32_t pd_shift;        // log2(pd) when pd is a power of two, else -1
-  int32_t reserved;
+  int32_t pitch;           // elements between consecutive panel lines (= pd: the reference layout;
+                           // wider: padded lines, the dual kernel's conflict-free D stages)
 };
 
 // Exact (reference-replaying) gemm modes.
@@ -148,7 +149,7 @@ struct DualDesc {
   int32_t nd, nf;            // jobs per group
   int32_t tiles_d, tiles_f;  // virtual tiles per group
   int32_t prefetch_c;        // producers warm L2 with each tile's C
-  int32_t pad0;
+  int32_t sleep_ns;          // suspend-time hint of the producers' empty-slot waits (0: spin)
   unsigned long long* timing;  // tuning only: {~first start, D end, F end} (%globaltimer ns, max-reduced) or null
   int* counters;               // {D, F} tile counters, zero before the launch (dynamic tiles), or null
   DualJob d[DUAL_MAX_JOBS];
@@ -192,6 +193,9 @@ int dmma_ctas_per_sm(const FastTile& t, int cdt);
 int ffma_ctas_per_sm(const FastTile& t, int cdt);
 // Dual-pipe kernel: one CTA per SM (grid), D and F groups on their job lists.
 size_t dual_smem();
+// Line pitch (doubles) of the D jobs' packed panels: the D group's smem
+// stage pitch (MDGEMM_DUAL_PAD tuning: 128 + pad).
+int dual_d_pitch();
 cudaError_t launch_gemm_dual(const DualDesc& d, int grid, cudaStream_t s);
 // Split-K: sum the `splits` partial tiles in split order and run the fused
 // epilogue (one CTA per tile).

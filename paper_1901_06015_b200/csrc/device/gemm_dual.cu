@@ -51,20 +51,22 @@ constexpr int DF_BM = 64, DF_BN = 128;   // F tile; 128 threads (8 x 16) of 8x8
 // 32 banks of a half-warp once.  With the packed pitch of 128 the four tig
 // lines of a half-warp fall on the same banks (4-way conflicts; ncu: 48 % of
 // the shared-load wavefronts of the step were conflicts).
-constexpr int DD_P = DD_BM + 4;
 static_assert(DD_BM == DD_BN, "one line pitch for both D operands");
-constexpr int DD_SA = DU_BK * DD_P, DD_SB = DU_BK * DD_P;  // doubles per stage (padded lines)
+template <int PAD>
+struct DPitch {
+  static constexpr int P = DD_BM + PAD;           // smem line pitch (doubles)
+  static constexpr int SA = DU_BK * P, SB = DU_BK * P;  // doubles per stage
+};
 constexpr int DF_SA = DF_BK * DF_BM, DF_SB = DF_BK * DF_BN;  // floats per stage
 constexpr int DD_WARPS = 8, DF_WARPS = 4;
-template <int DD_STAGES, int DF_STAGES>
+template <int DD_STAGES, int DF_STAGES, int PAD = 4>
 struct DuRings {
-  static constexpr size_t DD_RING = size_t(DD_STAGES) * (DD_SA + DD_SB) * sizeof(double);
+  static constexpr size_t DD_RING = size_t(DD_STAGES) * (DPitch<PAD>::SA + DPitch<PAD>::SB) * sizeof(double);
   static constexpr size_t DF_RING = size_t(DF_STAGES) * (DF_SA + DF_SB) * sizeof(float);
   static constexpr size_t SMEM =
       DD_RING + DF_RING + (2 * DD_STAGES + 2 * DF_STAGES) * sizeof(uint64_t) + (DD_STAGES + DF_STAGES + DD_WARPS + DF_WARPS) * sizeof(int);
 };
 constexpr int DU_THREADS = 512;
-constexpr uint32_t kSleepNs = 20000;  // suspend-time hint of the producers' empty-slot waits
 constexpr int DD_PROD_WARP = 12, DF_PROD_WARP = 13;
 
 // %laneid == 0, read where it is needed (ptxas otherwise keeps `lane` live
@@ -284,10 +286,12 @@ __device__ __forceinline__ void prefetch_c(const DualJob& jb, int tm, int tn, in
 
 // Register split per warp group (setmaxnreg): RP producers, RD DMMA warps,
 // RF FFMA2 warps; RP*128 + RD*256 + RF*128 = the CTA's launch allocation.
-template <int DD_STAGES, int DF_STAGES, int RP, int RD, int RF>
+template <int DD_STAGES, int DF_STAGES, int PAD, int RP, int RD, int RF>
 __device__ __forceinline__ void dual_body(const DualDesc& d) {
-  constexpr size_t DD_RING = DuRings<DD_STAGES, DF_STAGES>::DD_RING;
-  constexpr size_t DF_RING = DuRings<DD_STAGES, DF_STAGES>::DF_RING;
+  constexpr size_t DD_RING = DuRings<DD_STAGES, DF_STAGES, PAD>::DD_RING;
+  constexpr size_t DF_RING = DuRings<DD_STAGES, DF_STAGES, PAD>::DF_RING;
+  constexpr int DD_P = DPitch<PAD>::P, DD_SA = DPitch<PAD>::SA, DD_SB = DPitch<PAD>::SB;
+  const uint32_t sleep_ns = static_cast<uint32_t>(d.sleep_ns);  // producers' empty-slot waits (0: spin)
   extern __shared__ __align__(128) unsigned char smem[];
   double* dA = reinterpret_cast<double*>(smem);
   double* dB = dA + DD_STAGES * DD_SA;
@@ -324,11 +328,12 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     // first, so CTAs that finish early take the next longest: balanced tails),
     // else the static boustrophedon rounds.  The producer hands the tile to
     // its consumers in the first stage's slot; -1 ends the list.
-    // P: smem line pitch of a stage (elements); P == BM: one copy per operand
-    // and stage, else one copy per k-line into padded lines
+    // A stage is BK panel lines of the packed operands (SA / BK and SB / BK
+    // elements each: the panel dimension, or the D group's padded pitch), one
+    // contiguous bulk copy per operand
     auto run_producer = [&](auto* A, auto* B, uint64_t* full, uint64_t* empty, int* slot, const DualJob* jobs,
                             int njobs, int tiles, int* counter, int STAGES, int BM, int BN, int SA, int SB, int BK,
-                            int P, int esz) {
+                            int esz) {
       using T = typename std::remove_pointer<decltype(A)>::type;
       int it = 0;
       auto next = [&](int r) -> int {
@@ -345,7 +350,7 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         const int v = next(r);
         if (v >= tiles) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, sleep_ns);
           slot[s] = -1;
           mbar_arrive(&full[s]);
           return;
@@ -354,30 +359,22 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         int tm, tn;
         tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
         if (d.prefetch_c) prefetch_c(jb, tm, tn, BM, BN);
-        const T* Ag = static_cast<const T*>(jb.a) + static_cast<int64_t>(tm) * BM * jb.lpad;
-        const T* Bg = static_cast<const T*>(jb.b) + static_cast<int64_t>(tn) * BN * jb.lpad;
+        // panels of SA / BK (SB / BK) elements per line
+        const T* Ag = static_cast<const T*>(jb.a) + static_cast<int64_t>(tm) * (SA / BK) * jb.lpad;
+        const T* Bg = static_cast<const T*>(jb.b) + static_cast<int64_t>(tn) * (SB / BK) * jb.lpad;
         const int nk = static_cast<int>(jb.lpad / BK);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, sleep_ns);
           // stage word: the tile (2v) on its first k-block, bit 0 on its last
           slot[s] = (kb == 0 ? 2 * v : 0) | (kb == nk - 1 ? 1 : 0);
-          mbar_arrive_expect_tx(&full[s], (BM + BN) * BK * esz);
-          const T* ak = Ag + static_cast<int64_t>(kb) * BK * BM;
-          const T* bk = Bg + static_cast<int64_t>(kb) * BK * BN;
-          if (P == BM) {
-            bulk_g2s(A + s * SA, ak, BK * BM * esz, &full[s]);
-            bulk_g2s(B + s * SB, bk, BK * BN * esz, &full[s]);
-          } else {
-            for (int l = 0; l < BK; ++l) {
-              bulk_g2s(A + s * SA + l * P, ak + l * BM, BM * esz, &full[s]);
-              bulk_g2s(B + s * SB + l * P, bk + l * BN, BN * esz, &full[s]);
-            }
-          }
+          mbar_arrive_expect_tx(&full[s], (SA + SB) * esz);
+          bulk_g2s(A + s * SA, Ag + static_cast<int64_t>(kb) * SA, SA * esz, &full[s]);
+          bulk_g2s(B + s * SB, Bg + static_cast<int64_t>(kb) * SB, SB * esz, &full[s]);
         }
         if (!counter && (r + 1) * G >= tiles) {  // static order: done after the last round
           const int s = it % STAGES;
-          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, kSleepNs);
+          if (it >= STAGES) mbar_wait_sleep_u32(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1, sleep_ns);
           slot[s] = -1;
           mbar_arrive(&full[s]);
           return;
@@ -386,10 +383,10 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
     };
     if (warp == DD_PROD_WARP)
       run_producer(dA, dB, dfull, dempty, dslot, d.d, d.nd, d.tiles_d, d.counters ? d.counters : nullptr, DD_STAGES,
-                   DD_BM, DD_BN, DD_SA, DD_SB, DU_BK, DD_P, static_cast<int>(sizeof(double)));
+                   DD_BM, DD_BN, DD_SA, DD_SB, DU_BK, static_cast<int>(sizeof(double)));
     else if (warp == DF_PROD_WARP)
       run_producer(fA, fB, ffull, fempty, fslot, d.f, d.nf, d.tiles_f, d.counters ? d.counters + 1 : nullptr,
-                   DF_STAGES, DF_BM, DF_BN, DF_SA, DF_SB, DF_BK, DF_BM, static_cast<int>(sizeof(float)));
+                   DF_STAGES, DF_BM, DF_BN, DF_SA, DF_SB, DF_BK, static_cast<int>(sizeof(float)));
     return;
   }
 
@@ -514,15 +511,15 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
 
 // The whole register file (128 per thread at launch: 256 x 168 + 128 x 144 +
 // 128 x 32 = 64 K).
-template <int DD_STAGES, int DF_STAGES>
+template <int DD_STAGES, int DF_STAGES, int PAD>
 __global__ void __launch_bounds__(DU_THREADS, 1) gemm_dual_kernel(const __grid_constant__ DualDesc d) {
-  dual_body<DD_STAGES, DF_STAGES, 32, 168, 144>(d);
+  dual_body<DD_STAGES, DF_STAGES, PAD, 32, 168, 144>(d);
 }
 
-template <int DS, int FS>
+template <int DS, int FS, int PAD>
 cudaError_t launch_stages(const DualDesc& d, int grid, cudaStream_t s) {
-  constexpr size_t smem = DuRings<DS, FS>::SMEM;
-  auto kern = gemm_dual_kernel<DS, FS>;
+  constexpr size_t smem = DuRings<DS, FS, PAD>::SMEM;
+  auto kern = gemm_dual_kernel<DS, FS, PAD>;
   cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
   kern<<<static_cast<unsigned>(grid), DU_THREADS, smem, s>>>(d);
@@ -533,14 +530,25 @@ cudaError_t launch_stages(const DualDesc& d, int grid, cudaStream_t s) {
 
 size_t dual_smem() { return DuRings<3, 4>::SMEM; }
 
+static int dual_pad() {  // tuning: MDGEMM_DUAL_PAD = 0 packed D line pitch (4-way bank conflicts)
+  static const int pad = [] {
+    const char* f = std::getenv("MDGEMM_DUAL_PAD");
+    return f && std::atoi(f) == 0 ? 0 : 4;
+  }();
+  return pad;
+}
+
+int dual_d_pitch() { return DD_BM + dual_pad(); }
+
 cudaError_t launch_gemm_dual(const DualDesc& d, int grid, cudaStream_t s) {
   if (grid <= 0 || (d.tiles_d == 0 && d.tiles_f == 0)) return cudaSuccess;
   static const int variant = [] {  // tuning: MDGEMM_DUAL_STAGES = 0 (3 D / 4 F), 1 (3 / 5)
     const char* f = std::getenv("MDGEMM_DUAL_STAGES");
     return f ? std::atoi(f) : 0;
   }();
-  if (variant == 1) return launch_stages<3, 5>(d, grid, s);
-  return launch_stages<3, 4>(d, grid, s);
+  if (dual_pad() == 0) return launch_stages<3, 4, 0>(d, grid, s);
+  if (variant == 1) return launch_stages<3, 5, 4>(d, grid, s);
+  return launch_stages<3, 4, 4>(d, grid, s);
 }
 
 }  // namespace mdg

@@ -72,9 +72,9 @@ cudaError_t pad(const PackDesc& d, void* dst, cudaStream_t s) {
   if (d.lpad <= d.len || d.panels == 0) return cudaSuccess;
   // Zero the inner-dimension padding rows [len, lpad) of every panel.
   const size_t esz = (d.target_single ? 4 : 8) * (d.out_complex ? 2 : 1);
-  const size_t pitch = static_cast<size_t>(d.pd * d.lpad) * esz;
-  const size_t width = static_cast<size_t>(d.pd * (d.lpad - d.len)) * esz;
-  char* first = static_cast<char*>(dst) + static_cast<size_t>(d.pd * d.len) * esz;
+  const size_t pitch = static_cast<size_t>(d.pitch * d.lpad) * esz;
+  const size_t width = static_cast<size_t>(d.pitch * (d.lpad - d.len)) * esz;
+  char* first = static_cast<char*>(dst) + static_cast<size_t>(d.pitch * d.len) * esz;
   return cudaMemset2DAsync(first, pitch, 0, width, static_cast<size_t>(d.panels), s);
 }
 

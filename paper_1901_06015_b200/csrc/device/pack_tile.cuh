@@ -78,7 +78,7 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
   sync();
 
   // Store: coalesce along the packed buffer's contiguous axis.
-  const int64_t PD = d.pd, LP = d.lpad;
+  const int64_t PD = d.pd, LP = d.lpad, PT = d.pitch;
 #pragma unroll
   for (int r = 0; r < TILE / ROWS; ++r) {
     const int ii = SIDE == MDG_SIDE_LEFT ? lane : row + ROWS * r;
@@ -91,8 +91,8 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
     const int sh = d.pd_shift;
     auto off = [&](int64_t pr, int64_t pc) -> int64_t {
       const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
-      if (sh >= 0) return ((x >> sh) * LP + y) * PD + (x & (PD - 1));
-      return (x / PD) * PD * LP + y * PD + x % PD;
+      if (sh >= 0) return ((x >> sh) * LP + y) * PT + (x & (PD - 1));
+      return (x / PD) * PT * LP + y * PT + x % PD;
     };
     if constexpr (FMT == MDG_FMT_STANDARD) {
       if constexpr (SRC_COMPLEX) {

@@ -116,11 +116,14 @@ struct Packed {
   size_t bytes = 0;
 };
 
+// pitch: real elements between consecutive panel lines (0: the tile, the
+// reference layout)
 Packed prepare_pack(const MatrixView& src, Side side, PackFormat fmt, bool conj, const Scalar& scale,
-                    Datatype target, int64_t tile, int64_t lpad) {
+                    Datatype target, int64_t tile, int64_t lpad, int64_t pitch = 0) {
   const bool halves = fmt == PackFormat::Standard && src.dtype.domain == Domain::Complex;
   Packed out;
-  out.desc = make_pack_desc(src, side, fmt, conj, scale, target, halves ? tile / 2 : tile, lpad, &out.bytes);
+  out.desc = make_pack_desc(src, side, fmt, conj, scale, target, halves ? tile / 2 : tile, lpad, &out.bytes,
+                            halves ? pitch / 2 : pitch);
   return out;
 }
 
@@ -150,24 +153,26 @@ bool onem_direct(const ExecutionPlan& p);
 
 }  // namespace
 
-// FAST per-KC-block structure of a plan without C_temp: 0 none (one combine
-// after the full inner dimension is exact for C_temp plans and the Direct
-// paths: they accumulate continuously in the computation precision), 1 one
-// combine per KC block (Temp path), 2 the first KC block then the rest (1m
-// with a complex beta).  Odd KC blocks of a 1m image would split a complex
-// element's real and imaginary steps; those plans keep one combine.
+// FAST per-KC-block structure of a plan without C_temp: 0 one combine after
+// the full inner dimension, 1 one combine per KC block.  The reference's
+// Temp / 1m-temp routes round each KC block's sum into C (gemm_core.cpp:
+// 125-127); that changes the values only where C is stored at another
+// precision than the computation's (each block meets C's rounding, or C's
+// wider accumulation).  Where the two precisions agree, the block boundaries
+// only reorder the sum in the computation precision -- within the bound FAST
+// already meets -- and the call keeps one pass (and the dual kernel).  C_temp
+// plans and the Direct paths accumulate continuously: one combine.  Odd KC
+// blocks of a 1m image would split a complex element's real and imaginary
+// steps; those plans keep one combine too.
 int fast_block_mode(const ExecutionPlan& p, int64_t* f_a, int64_t* f_b) {
   if (p.ctemp || p.k <= p.params.kc || p.params.kc < 1) return 0;
+  if (p.c.dtype.precision == p.comp_prec) return 0;
   const int64_t fa = k_factor(p.format_a), fb = k_factor(p.format_b);
   if (p.params.kc % fa || p.params.kc % fb) return 0;
   int mode = 0;
   const bool onem = p.ukr_path == UkrPath::OneMColumn || p.ukr_path == UkrPath::OneMRow;
   if (p.ukr_path == UkrPath::Temp) mode = 1;
-  if (onem && !onem_direct(p)) {
-    const FlattenAxis ax = p.ukr_path == UkrPath::OneMColumn ? FlattenAxis::Rows : FlattenAxis::Cols;
-    const bool flat = p.c.dtype.precision == p.comp_prec && can_flatten(p.c, ax);
-    mode = flat ? 2 : 1;  // complex beta on a flattenable C: virtual_ukr_onem's mixed route
-  }
+  if (onem && !onem_direct(p)) mode = 1;  // C of another precision: virtual_ukr_temp per block
   if (f_a) *f_a = fa;
   if (f_b) *f_b = fb;
   return mode;
@@ -191,8 +196,9 @@ mdg::DView to_dview(const MatrixView& v) {
 }
 
 PackGeometry pack_geometry(const MatrixView& src, Side side, PackFormat format, Datatype target,
-                           int64_t reg_block, int64_t panel_len) {
+                           int64_t reg_block, int64_t panel_len, int64_t pitch) {
   if (reg_block < 1) throw Error("pack_block: reg_block must be at least 1");
+  if (pitch != 0 && pitch < reg_block) throw Error("pack_block: line pitch below the panel dimension");
   const bool left = side == Side::Left;
   PackGeometry g;
   int64_t rows = 0, cols = 0;
@@ -221,7 +227,8 @@ PackGeometry pack_geometry(const MatrixView& src, Side side, PackFormat format, 
   g.panels = (extent + reg_block - 1) / reg_block;
   g.len = left ? cols : rows;
   g.lpad = std::max(g.len, panel_len);
-  g.bytes = static_cast<size_t>(g.panels * reg_block * g.lpad) * dtype_size(g.block_dtype);
+  g.pitch = pitch ? pitch : reg_block;
+  g.bytes = static_cast<size_t>(g.panels * g.pitch * g.lpad) * dtype_size(g.block_dtype);
   return g;
 }
 
@@ -250,10 +257,10 @@ void pack_block_device(void* dst, const MatrixView& src, Side side, PackFormat f
 
 mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format, bool conj,
                              const Scalar& scale, Datatype target, int64_t reg_block, int64_t panel_len,
-                             size_t* bytes) {
+                             size_t* bytes, int64_t pitch) {
   if (scale.im != 0.0 && format == PackFormat::Standard)
     throw Error("pack_block: complex scale requires OneE or OneR format");
-  const PackGeometry g = pack_geometry(src, side, format, target, reg_block, panel_len);
+  const PackGeometry g = pack_geometry(src, side, format, target, reg_block, panel_len, pitch);
   mdg::PackDesc d{};
   d.src = to_dview(src);
   d.side = side == Side::Left ? MDG_SIDE_LEFT : MDG_SIDE_RIGHT;
@@ -265,6 +272,7 @@ mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format
   d.target_single = target.precision == Precision::Single;
   d.out_complex = g.block_dtype.domain == Domain::Complex;
   d.pd = reg_block;
+  d.pitch = static_cast<int32_t>(g.pitch);
   d.pd_shift = -1;
   if ((reg_block & (reg_block - 1)) == 0)
     for (int s = 0; s < 63; ++s)
@@ -433,12 +441,11 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
   const bool exact = numerics == Numerics::Exact;
   const int sms = device_sms();
 
-  // ctemp.enable = off (or auto with several threads) on a Temp-path plan: the
-  // reference rounds each KC block's partial sum into C (gemm_core.cpp:125-127,
+  // ctemp.enable = off (or auto with several threads) on a Temp-path plan with
+  // C stored at another precision than the computation's: the reference
+  // rounds each KC block's partial sum into C (gemm_core.cpp:125-127,
   // kernels.cpp:97-132).  FAST keeps that structure: one kernel pass per KC
-  // block of the real inner dimension, beta on the first and 1 afterwards
-  // (1m with a complex beta: the first block, then the rest in one pass,
-  // kernels.cpp:141-150).
+  // block of the real inner dimension, beta on the first and 1 afterwards.
   if (!exact && block_split) {
     int64_t f_a = 1, f_b = 1;
     const int mode = fast_block_mode(p, &f_a, &f_b);
@@ -450,7 +457,7 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
         return;
       }
       for (int64_t pc = 0; pc < p.k;) {
-        const int64_t hi = mode == 2 && pc > 0 ? p.k : std::min(pc + kc, p.k);
+        const int64_t hi = std::min(pc + kc, p.k);
         ExecutionPlan q = k_slice(p, pc, hi, f_a, f_b);
         if (pc > 0) q.beta = Scalar{1.0, 0.0, p.beta.dtype};
         execute_scheduled(q, numerics, stream_ptr, nullptr, shared, arena, arena_bytes, nullptr, allow_splitk, false,
@@ -727,8 +734,13 @@ DualPrep dual_prepare(const ExecutionPlan& p) {
   const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
   const int64_t bk = d.single ? mdg::DUAL_F_BK : mdg::DUAL_BK;
   d.lpad = (p.k + bk - 1) / bk * bk;
-  const Packed pa = prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, bm, d.lpad);
-  const Packed pb = prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, bn, d.lpad);
+  // D jobs: panel lines at the dual kernel's conflict-free smem pitch, so a
+  // stage stays one contiguous bulk copy per operand
+  const int64_t pitch = d.single ? 0 : mdg::dual_d_pitch();
+  const Packed pa =
+      prepare_pack(p.a, Side::Left, p.format_a, p.conj_a, p.pack_scale_a, p.target_dtype_a, bm, d.lpad, pitch);
+  const Packed pb =
+      prepare_pack(p.b, Side::Right, p.format_b, p.conj_b, p.pack_scale_b, p.target_dtype_b, bn, d.lpad, pitch);
   d.pa = pa.desc;
   d.pb = pb.desc;
   d.bytes_a = pa.bytes;
@@ -779,6 +791,11 @@ void dual_launch(const mdg::DualDesc& desc, double flops_d, double flops_f, cuda
     return f ? std::atoi(f) : 1;
   }();
   d.prefetch_c = prefetch;
+  static const int sleep_ns = [] {  // tuning: MDGEMM_DUAL_SLEEP = suspend hint in ns (0: spinning waits)
+    const char* f = std::getenv("MDGEMM_DUAL_SLEEP");
+    return f ? std::atoi(f) : 20000;
+  }();
+  d.sleep_ns = sleep_ns;
   prof::Scope scope(MDG_KERNEL_DUAL_D, st, flops_d, MDG_KERNEL_DUAL_F, flops_f);
   cuda_check(mdg::launch_gemm_dual(d, device_sms(), st), "dual-pipe gemm kernel");
 }

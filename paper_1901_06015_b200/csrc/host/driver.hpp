@@ -40,14 +40,15 @@ struct PackGeometry {
   int64_t panels = 0;
   int64_t len = 0;   // logical panel length
   int64_t lpad = 0;  // allocated panel length
+  int64_t pitch = 0; // elements between consecutive panel lines (>= reg_block)
   size_t bytes = 0;
 };
 PackGeometry pack_geometry(const MatrixView& src, Side side, PackFormat format, Datatype target,
-                           int64_t reg_block, int64_t panel_len);
+                           int64_t reg_block, int64_t panel_len, int64_t pitch = 0);
 
 mdg::PackDesc make_pack_desc(const MatrixView& src, Side side, PackFormat format, bool conj,
                              const Scalar& scale, Datatype target, int64_t reg_block, int64_t panel_len,
-                             size_t* bytes);
+                             size_t* bytes, int64_t pitch = 0);
 
 void pack_block_device_padded(void* dst, const MatrixView& src, Side side, PackFormat format, bool conj,
                               Scalar scale, Datatype target, int64_t reg_block, int64_t panel_len,
@@ -107,8 +108,8 @@ struct DualPiece {
 std::vector<DualPiece> dual_schedule_pieces(const std::vector<GemmCall>& calls, const Config& cfg,
                                             std::vector<int32_t>* call_tiles);
 
-// FAST numerics of a plan without C_temp whose Temp / 1m route rounds into C
-// per KC block: 0 none, 1 per KC block, 2 first block then the rest (see
+// FAST numerics of a plan without C_temp whose Temp / 1m route rounds into a
+// C of another precision per KC block: 0 one combine, 1 per KC block (see
 // driver.cpp); f_a / f_b receive the real inner steps per source column / row.
 int fast_block_mode(const ExecutionPlan& p, int64_t* f_a = nullptr, int64_t* f_b = nullptr);
 

@@ -168,6 +168,7 @@ def rel_frobenius(got: np.ndarray, want: np.ndarray) -> float:
 
 def ulp_distance(got: np.ndarray, want: np.ndarray) -> np.ndarray:
     """Per-component distance in units of the storage precision's ulp."""
+    got, want = np.ascontiguousarray(got), np.ascontiguousarray(want)
     g = got.view(np.float32 if got.dtype in (np.float32, np.complex64) else np.float64)
     w = want.view(g.dtype)
     itype = np.int32 if g.dtype == np.float32 else np.int64

@@ -4,9 +4,11 @@ Without C_temp the reference rounds each KC block's partial sum into C
 (Temp path: one accumulate_element per block, beta on the first and 1 after,
 gemm_core.cpp:125-127, kernels.cpp:97-132; 1m with a complex beta: the first
 block through the temp tile, the rest continued in the computation precision,
-kernels.cpp:141-150).  FAST runs one kernel pass per KC block (driver.cpp:
+kernels.cpp:141-150).  Where C is stored at another precision than the
+computation's, FAST runs one kernel pass per KC block (driver.cpp:
 fast_block_mode), so each block's sum meets C's storage rounding exactly where
-the reference's does.  Checked against the oracle run with the same Config
+the reference's does; where the precisions agree the block boundaries only
+reorder the sum in the computation precision and FAST keeps one pass.  Checked against the oracle run with the same Config
 (per-element criterion, north-star Frobenius bound) and against EXACT: where
 C's storage precision is narrower than the computation precision (the
 per-block sums are rounded to storage), every element is within one storage
