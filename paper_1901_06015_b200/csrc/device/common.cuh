@@ -569,10 +569,26 @@ struct Sched {
   int end_tile, end_k0;      // SEG_END (end_k0 == 0: none)
 };
 
+// Stream-K CTAs wait for their predecessor's published partial tile, so the
+// order of the CTA numbers must be an order in which CTAs START: a CTA takes
+// its logical number from a ticket counter (zeroed with the publish flags)
+// when it begins, so CTA b-1 is already running -- and finishes its first
+// segment without waiting on anyone -- before CTA b can wait for it, however
+// the hardware dispatches the grid or shares the SMs with other kernels.
+// No ticket (no range splits a tile): the block index.
+__device__ __forceinline__ int logical_cta(int* ticket) {
+  __shared__ int cta;
+  if (threadIdx.x == 0) cta = ticket ? atomicAdd(ticket, 1) : static_cast<int>(blockIdx.x);
+  __syncthreads();
+  return cta;
+}
+__device__ __forceinline__ int* sk_ticket(const GemmDesc& d) { return d.sk_flags ? d.sk_flags + d.sk_grid : nullptr; }
+
 // SK is a template flag so the classic kernels compile to one straight
-// segment (the segment loop costs registers).
+// segment (the segment loop costs registers).  cta: the logical CTA number
+// (logical_cta) of a stream-K launch.
 template <bool SK>
-__device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, int nk) {
+__device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, int nk, int cta) {
   Sched s{};
   s.tiles = static_cast<int>(tiles);
   s.nk = nk;
@@ -580,9 +596,9 @@ __device__ __forceinline__ Sched make_sched(const GemmDesc& d, int64_t tiles, in
   s.nseg = 1;
   if (!SK) return s;
   const int64_t G = d.sk_grid, dp = sk_dp_tiles(tiles, G);
-  const int64_t b = static_cast<int64_t>(blockIdx.x) - dp;
+  const int64_t b = static_cast<int64_t>(cta) - dp;
   if (b < 0) {  // a whole tile
-    s.full0 = static_cast<int>(blockIdx.x);
+    s.full0 = cta;
     s.start_tile = s.full0 + 1;
     return s;
   }

@@ -108,7 +108,7 @@ struct GemmDesc {
   void* partials;      // splits > 1: per (tile, split) accumulator tiles, comp precision
   unsigned long long* trace;  // tuning only (MDGEMM_TRACE): TRACE_WORDS stamps per CTA
   void* sk_partials;   // stream-K: sk_grid partial tiles in thread-fragment order, comp precision
-  int* sk_flags;       // stream-K: sk_grid publish flags, zeroed before the launch
+  int* sk_flags;       // stream-K: sk_grid publish flags + the start ticket, zeroed before the launch
   int32_t c_prefetch;  // producer warms L2 with the C tile after its loads (short k)
   int32_t pad0;
 };

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
   const int tiles_n = static_cast<int>((d.ne + C::BN - 1) / C::BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
   const int64_t lpad = d.a.lpad;
-  const Sched sc = make_sched<SK>(d, tiles, static_cast<int>(lpad / C::BK));
+  const Sched sc = make_sched<SK>(d, tiles, static_cast<int>(lpad / C::BK), SK ? logical_cta(sk_ticket(d)) : 0);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned long long t_start = d.trace ? globaltimer() : 0;

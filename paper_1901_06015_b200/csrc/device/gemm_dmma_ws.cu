@@ -61,16 +61,18 @@ struct WsCfg {
 // (stream-K) the CTA's k-block range of the last G + tiles % G tiles.
 struct WsSched {
   int nk, nseg, dpw, G;
+  int b;                     // logical CTA number (logical_cta)
   int start_tile, start_k1;  // SEG_START (start_k1 == 0: none)
   int full0, full1;          // whole tiles of the range
   int end_tile, end_k0;      // SEG_END (end_k0 == 0: none)
 };
 
-__device__ __forceinline__ WsSched ws_sched(int64_t tiles, int nk, bool sk) {
+__device__ __forceinline__ WsSched ws_sched(int64_t tiles, int nk, bool sk, int cta) {
   WsSched s{};
   s.nk = nk;
   s.G = static_cast<int>(gridDim.x);
-  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t G = gridDim.x, b = cta;
+  s.b = cta;
   const int64_t R = tiles % G;
   if (!sk || R == 0) {
     s.dpw = static_cast<int>((tiles - b + G - 1) / G);
@@ -97,7 +99,7 @@ __device__ __forceinline__ WsSched ws_sched(int64_t tiles, int nk, bool sk) {
 // range's whole tiles, SEG_END last.  CTA b+1 reaches its SEG_END no earlier
 // than CTA b finishes its SEG_START, since every range is >= one tile long.
 __device__ __forceinline__ Seg ws_seg(const WsSched& s, int idx) {
-  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
+  if (idx < s.dpw) return Seg{s.b + idx * s.G, 0, s.nk, SEG_FULL};
   idx -= s.dpw;
   if (s.start_k1 != 0) {
     if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
   const int tiles_n = static_cast<int>((d.ne + WS_BN - 1) / WS_BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
   const int64_t lpad = d.a.lpad;
-  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0);
+  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0, logical_cta(sk_ticket(d)));
 
   const DEpilogue& e = d.epi;
   const bool prow = e.pair == MDG_PAIR_ROWS, pcol = e.pair == MDG_PAIR_COLS;
@@ -275,10 +277,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
     const Seg sg = ws_seg(sc, si);
     double acc[WS_MT][WS_NT][2];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
-      if (tid == 0) flag_acquire_wait(d.sk_flags + blockIdx.x - 1);
+      if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, WS_MMA_THREADS);
       const double* slot =
-          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x - 1) * (WS_BM * WS_BN);
+          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(sc.b - 1) * (WS_BM * WS_BN);
 #pragma unroll
       for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
     }
     if (sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
-      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x) * (WS_BM * WS_BN);
+      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(sc.b) * (WS_BM * WS_BN);
 #pragma unroll
       for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
           for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
       __threadfence();
       named_sync(1, WS_MMA_THREADS);
-      if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
+      if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }
     // combine with this tile's C (already in ctile) in place.  The epilogue
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
   const int tiles_n = static_cast<int>((d.ne + WS_BN - 1) / WS_BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
   const int64_t lpad = d.a.lpad;
-  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0);
+  const WsSched sc = ws_sched(tiles, static_cast<int>(lpad / WS_BK), d.sk_grid > 0, logical_cta(sk_ticket(d)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (smem_u32(ctile) & 1023) __trap();  // the 128-byte swizzle needs 1 KB-aligned boxes
   if (threadIdx.x == 0) {
@@ -601,10 +603,10 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
     const Seg sg = ws_seg(sc, si);
     double acc[WS_MT][WS_NT][2];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
-      if (tid == 0) flag_acquire_wait(d.sk_flags + blockIdx.x - 1);
+      if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, WS_MMA_THREADS);
       const double* slot =
-          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x - 1) * (WS_BM * WS_BN);
+          static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(sc.b - 1) * (WS_BM * WS_BN);
 #pragma unroll
       for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
       if (lane == 0) mbar_arrive_u32(empty_u + 8 * s);
     }
     if (sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
-      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x) * (WS_BM * WS_BN);
+      double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(sc.b) * (WS_BM * WS_BN);
 #pragma unroll
       for (int i = 0; i < WS_MT; ++i)
 #pragma unroll
@@ -649,7 +651,7 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
           for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
       __threadfence();
       named_sync(1, WS_MMA_THREADS);
-      if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
+      if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }
     // round to C's precision (accumulate_element's tc) into the stage buffer

@@ -46,16 +46,18 @@ struct FwCfg {
 
 struct FwSched {
   int nk, nseg, dpw, G;
+  int b;                     // logical CTA number (logical_cta)
   int start_tile, start_k1;
   int full0, full1;
   int end_tile, end_k0;
 };
 
-__device__ __forceinline__ FwSched fw_sched(int64_t tiles, int nk, bool sk) {
+__device__ __forceinline__ FwSched fw_sched(int64_t tiles, int nk, bool sk, int cta) {
   FwSched s{};
   s.nk = nk;
   s.G = static_cast<int>(gridDim.x);
-  const int64_t G = gridDim.x, b = blockIdx.x;
+  const int64_t G = gridDim.x, b = cta;
+  s.b = cta;
   const int64_t R = tiles % G;
   if (!sk || R == 0) {
     s.dpw = static_cast<int>((tiles - b + G - 1) / G);
@@ -79,7 +81,7 @@ __device__ __forceinline__ FwSched fw_sched(int64_t tiles, int nk, bool sk) {
 // whole-tile waves first (in step across CTAs), then the stream-K range
 // (see gemm_dmma_ws.cu: ws_seg)
 __device__ __forceinline__ Seg fw_seg(const FwSched& s, int idx) {
-  if (idx < s.dpw) return Seg{static_cast<int>(blockIdx.x) + idx * s.G, 0, s.nk, SEG_FULL};
+  if (idx < s.dpw) return Seg{s.b + idx * s.G, 0, s.nk, SEG_FULL};
   idx -= s.dpw;
   if (s.start_k1 != 0) {
     if (idx == 0) return Seg{s.start_tile, 0, s.start_k1, SEG_START};
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
   const int tiles_n = static_cast<int>((d.ne + FW_BN - 1) / FW_BN);
   const int64_t tiles = static_cast<int64_t>(tiles_m) * tiles_n;
   const int64_t lpad = d.a.lpad;
-  const FwSched sc = fw_sched(tiles, static_cast<int>(lpad / FW_BK), d.sk_grid > 0);
+  const FwSched sc = fw_sched(tiles, static_cast<int>(lpad / FW_BK), d.sk_grid > 0, logical_cta(sk_ticket(d)));
 
   const DEpilogue& e = d.epi;
   const bool prow = e.pair == MDG_PAIR_ROWS, pcol = e.pair == MDG_PAIR_COLS;
@@ -210,10 +212,10 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
     const Seg sg = fw_seg(sc, si);
     uint64_t acc[8][4];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
-      if (tid == 0) flag_acquire_wait(d.sk_flags + blockIdx.x - 1);
+      if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, FW_MMA_THREADS);
       const uint64_t* slot =
-          static_cast<const uint64_t*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x - 1) * (FW_BM * FW_BN / 2);
+          static_cast<const uint64_t*>(d.sk_partials) + static_cast<int64_t>(sc.b - 1) * (FW_BM * FW_BN / 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -251,14 +253,14 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
     }
     if (sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
       uint64_t* slot =
-          static_cast<uint64_t*>(d.sk_partials) + static_cast<int64_t>(blockIdx.x) * (FW_BM * FW_BN / 2);
+          static_cast<uint64_t*>(d.sk_partials) + static_cast<int64_t>(sc.b) * (FW_BM * FW_BN / 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int p = 0; p < 4; ++p) __stcg(slot + (i * 4 + p) * FW_MMA_THREADS + tid, acc[i][p]);
       __threadfence();
       named_sync(1, FW_MMA_THREADS);
-      if (tid == 0) flag_release(d.sk_flags + blockIdx.x);
+      if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }
     // combine with this tile's C (already in ctile) in place

@@ -97,6 +97,7 @@ void trim_workspace(size_t keep_bytes) {
   cuda_check(cudaDeviceSynchronize(), "trim_workspace: synchronize");
   cuda_check(cudaMemPoolTrimTo(workspace_pool(), keep_bytes), "cudaMemPoolTrimTo");
   reset_reservation();
+  if (keep_bytes == 0) trim_host_staging();
 }
 
 namespace {
@@ -563,7 +564,8 @@ void execute_scheduled(const ExecutionPlan& p, Numerics numerics, void* stream_p
                             : sk_ranges ? static_cast<size_t>(sk_grid) * tile.bm * tile.bn * acc_size
                                         : 0;
   const size_t off_f = off_p + (part_bytes + 255) / 256 * 256;
-  const size_t flag_bytes = sk_ranges ? static_cast<size_t>(sk_grid) * sizeof(int) : 0;  // publish flags
+  // publish flags + the start ticket (common.cuh: logical_cta)
+  const size_t flag_bytes = sk_ranges ? static_cast<size_t>(sk_grid + 1) * sizeof(int) : 0;
   if (ws_needed) {
     *ws_needed = off_f + flag_bytes;
     return;

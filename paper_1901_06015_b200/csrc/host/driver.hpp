@@ -32,6 +32,14 @@ void trim_workspace(size_t keep_bytes);
 // Forget the batch reservation (the pool was trimmed).
 void reset_reservation();
 
+// Operand copies between HBM and host memory (hostcopy.cpp): pageable host
+// memory goes through the library's pinned chunk ring (d2h_copy then returns
+// once the bytes are in place), pinned memory takes a plain async copy.
+bool host_pageable(const void* p);
+void h2d_copy(void* dst, const void* src, size_t n, cudaStream_t st);
+void d2h_copy(void* dst, const void* src, size_t n, cudaStream_t st);
+void trim_host_staging();
+
 mdg::DView to_dview(const MatrixView& v);
 
 // resolve_geometry (packing.cpp:27-67) plus an optional padded panel length.

@@ -558,12 +558,14 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
     for (size_t x = 0; x < all.size(); ++x) order[x] = x;
     std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return first_use[a] < first_use[b]; });
     std::vector<cudaEvent_t> staged(all.size(), nullptr);
+    std::vector<char> pageable_out(all.size(), 0);
+    for (size_t x = 0; x < all.size(); ++x) pageable_out[x] = last_write[x] >= 0 && host_pageable(all[x].lo);
     residents.resize(all.size());
     for (size_t x : order) {
       void* d = nullptr;
       cuda_check(ws_alloc(&d, all[x].bytes(), S.in), "staging allocation");
       residents[x] = {all[x], static_cast<std::byte*>(d)};
-      cuda_check(cudaMemcpyAsync(d, all[x].lo, all[x].bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
+      h2d_copy(d, all[x].lo, all[x].bytes(), S.in);
       g_h2d_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
       staged[x] = ev();
       cuda_check(cudaEventRecord(staged[x], S.in), "event");
@@ -690,20 +692,24 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
       }
       k_done[ui] = ev();
       cuda_check(cudaEventRecord(k_done[ui], K), "event");
-      // host results this launch wrote for the last time
+      // host results this launch wrote for the last time (pageable ones after
+      // the last launch: their copy-out holds the host thread)
       bool any = false;
       for (size_t x = 0; x < all.size(); ++x)
-        if (last_write[x] == static_cast<long>(ui)) {
+        if (last_write[x] == static_cast<long>(ui) && !pageable_out[x]) {
           if (!any) cuda_check(cudaStreamWaitEvent(S.out, k_done[ui], 0), "dependency");
           any = true;
-          cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(all[x].lo), residents[x].second, all[x].bytes(),
-                                     cudaMemcpyDeviceToHost, S.out),
-                     "D2H staging");
+          d2h_copy(const_cast<std::byte*>(all[x].lo), residents[x].second, all[x].bytes(), S.out);
           g_d2h_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
         }
     }
     // results back to the host (every host C, after the last launch), residents released
     cuda_check(cudaStreamWaitEvent(S.out, k_done.empty() ? fork : k_done.back(), 0), "join");
+    for (size_t x = 0; x < all.size(); ++x)
+      if (last_write[x] >= 0 && pageable_out[x]) {
+        d2h_copy(const_cast<std::byte*>(all[x].lo), residents[x].second, all[x].bytes(), S.out);
+        g_d2h_bytes.fetch_add(all[x].bytes(), std::memory_order_relaxed);
+      }
     for (auto& rs : residents) cuda_check(cudaFreeAsync(rs.second, S.out), "staging release");
     residents.clear();
     for (void*& a : arena)
@@ -849,8 +855,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
   auto write_back = [&](Resident& r) {
     if (!r.dirty) return;
     cuda_check(cudaStreamWaitEvent(S.out, cs[static_cast<size_t>(r.last_writer)].comp_done, 0), "dependency");
-    cuda_check(cudaMemcpyAsync(const_cast<std::byte*>(r.host.lo), r.dev, r.host.bytes(), cudaMemcpyDeviceToHost, S.out),
-               "D2H staging");
+    d2h_copy(const_cast<std::byte*>(r.host.lo), r.dev, r.host.bytes(), S.out);
     g_d2h_bytes.fetch_add(r.host.bytes(), std::memory_order_relaxed);
     r.dirty = false;
   };
@@ -930,7 +935,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
         void* d = nullptr;
         cuda_check(ws_alloc(&d, h.bytes(), S.in), "staging allocation");
         nr.dev = static_cast<std::byte*>(d);
-        cuda_check(cudaMemcpyAsync(d, h.lo, h.bytes(), cudaMemcpyHostToDevice, S.in), "H2D staging");
+        h2d_copy(d, h.lo, h.bytes(), S.in);
         g_h2d_bytes.fetch_add(h.bytes(), std::memory_order_relaxed);
         nr.staged = new_event();
         cuda_check(cudaEventRecord(nr.staged, S.in), "event");
