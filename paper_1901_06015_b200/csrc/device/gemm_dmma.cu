@@ -250,7 +250,7 @@ using Big = DmmaCfg<128, 128, 2, 4, 4>;
 // Two CTAs per SM (4 DMMA warps each, same 64x32 warp tiles): one CTA's
 // epilogue overlaps the other's mainloop.
 using Pair = DmmaCfg<64, 128, 1, 4, 4, 2>;
-using Small = DmmaCfg<64, 64, 2, 2, 4>;
+using Small = DmmaCfg<64, 64, 2, 2, 4, 3>;  // three per SM
 
 template <class C>
 int ctas_per_sm(int cdt) {

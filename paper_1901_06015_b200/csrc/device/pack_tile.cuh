@@ -53,8 +53,53 @@ struct Pair<double> {
   static __device__ __forceinline__ T make(double a, double b) { return make_double2(a, b); }
 };
 
+// Store one processed source element (i, j) -- packed-logical row / column
+// of the block -- in the panel layout of FMT / SIDE.
+template <typename D, bool SRC_COMPLEX, int FMT, int SIDE>
+__device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ dst, int64_t i, int64_t j, double2 v) {
+  const int64_t PD = d.pd, LP = d.lpad, PT = d.pitch;
+  // offset of packed-logical (pr, pc) in block elements; power-of-two panel
+  // dims (every kernel tile) avoid the 64-bit division per element
+  const int sh = d.pd_shift;
+  auto off = [&](int64_t pr, int64_t pc) -> int64_t {
+    const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
+    if (sh >= 0) return ((x >> sh) * LP + y) * PT + (x & (PD - 1));
+    return (x / PD) * PT * LP + y * PT + x % PD;
+  };
+  if constexpr (FMT == MDG_FMT_STANDARD) {
+    if constexpr (SRC_COMPLEX) {
+      reinterpret_cast<typename Pair<D>::T*>(dst)[off(i, j)] = Pair<D>::make(v.x, v.y);
+    } else {
+      dst[off(i, j)] = static_cast<D>(v.x);
+    }
+  } else if constexpr (FMT == MDG_FMT_ONEE) {
+    using P = typename Pair<D>::T;
+    if constexpr (SIDE == MDG_SIDE_LEFT) {
+      // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, -im], [im, re]]
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j + 1)) = Pair<D>::make(-v.y, v.x);
+    } else {
+      // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, im], [-im, re]]
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
+      *reinterpret_cast<P*>(dst + off(2 * i + 1, 2 * j)) = Pair<D>::make(-v.y, v.x);
+    }
+  } else {  // 1r
+    if constexpr (SIDE == MDG_SIDE_LEFT) {
+      dst[off(i, 2 * j)] = static_cast<D>(v.x);
+      dst[off(i, 2 * j + 1)] = static_cast<D>(v.y);
+    } else {
+      dst[off(2 * i, j)] = static_cast<D>(v.x);
+      dst[off(2 * i + 1, j)] = static_cast<D>(v.y);
+    }
+  }
+}
+
 // Tile `bid` (source tiles column-major over ext_i x ext_j) by NT threads
-// (thread t of NT); sync() separates the staging from the stores.
+// (thread t of NT); sync() separates the staging from the stores.  When the
+// source's unit-stride axis is the packed panels' contiguous axis (a left
+// pack of a column-major A, a right pack of a row-major B) the tile needs no
+// transpose: each element goes straight from its load to its store, both
+// coalesced, with no shared-memory round trip or barrier.
 template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE, int NT, class Sync>
 __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst, int64_t bid, Tile& tile, int t,
                                           Sync sync) {
@@ -63,9 +108,23 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
   const int64_t i0 = (bid % tiles_i) * TILE;
   const int64_t j0 = (bid / tiles_i) * TILE;
   const int lane = t & 31, row = t >> 5;
+  const bool i_fast = d.src.rs <= d.src.cs;
+
+  if (i_fast == (SIDE == MDG_SIDE_LEFT)) {  // no transpose (uniform per launch)
+#pragma unroll
+    for (int r = 0; r < TILE / ROWS; ++r) {
+      const int ii = i_fast ? lane : row + ROWS * r;
+      const int jj = i_fast ? row + ROWS * r : lane;
+      const int64_t i = i0 + ii, j = j0 + jj;
+      if (i >= d.ext_i || j >= d.ext_j) continue;
+      double2 v = make_double2(0.0, 0.0);  // padded slots take literal zeros
+      if (i < d.src.m && j < d.src.n) v = process(load_src<S, SRC_COMPLEX>(d.src, i, j), d);
+      put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, v);
+    }
+    return;
+  }
 
   // Load: coalesce along the source's unit-stride axis.
-  const bool i_fast = d.src.rs <= d.src.cs;
 #pragma unroll
   for (int r = 0; r < TILE / ROWS; ++r) {
     const int ii = i_fast ? lane : row + ROWS * r;
@@ -78,48 +137,13 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
   sync();
 
   // Store: coalesce along the packed buffer's contiguous axis.
-  const int64_t PD = d.pd, LP = d.lpad, PT = d.pitch;
 #pragma unroll
   for (int r = 0; r < TILE / ROWS; ++r) {
     const int ii = SIDE == MDG_SIDE_LEFT ? lane : row + ROWS * r;
     const int jj = SIDE == MDG_SIDE_LEFT ? row + ROWS * r : lane;
     const int64_t i = i0 + ii, j = j0 + jj;
     if (i >= d.ext_i || j >= d.ext_j) continue;
-    const double2 v = tile[jj][ii];
-    // offset of packed-logical (pr, pc) in block elements; power-of-two panel
-    // dims (every kernel tile) avoid the 64-bit division per element
-    const int sh = d.pd_shift;
-    auto off = [&](int64_t pr, int64_t pc) -> int64_t {
-      const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
-      if (sh >= 0) return ((x >> sh) * LP + y) * PT + (x & (PD - 1));
-      return (x / PD) * PT * LP + y * PT + x % PD;
-    };
-    if constexpr (FMT == MDG_FMT_STANDARD) {
-      if constexpr (SRC_COMPLEX) {
-        reinterpret_cast<typename Pair<D>::T*>(dst)[off(i, j)] = Pair<D>::make(v.x, v.y);
-      } else {
-        dst[off(i, j)] = static_cast<D>(v.x);
-      }
-    } else if constexpr (FMT == MDG_FMT_ONEE) {
-      using P = typename Pair<D>::T;
-      if constexpr (SIDE == MDG_SIDE_LEFT) {
-        // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, -im], [im, re]]
-        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
-        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j + 1)) = Pair<D>::make(-v.y, v.x);
-      } else {
-        // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, im], [-im, re]]
-        *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
-        *reinterpret_cast<P*>(dst + off(2 * i + 1, 2 * j)) = Pair<D>::make(-v.y, v.x);
-      }
-    } else {  // 1r
-      if constexpr (SIDE == MDG_SIDE_LEFT) {
-        dst[off(i, 2 * j)] = static_cast<D>(v.x);
-        dst[off(i, 2 * j + 1)] = static_cast<D>(v.y);
-      } else {
-        dst[off(2 * i, j)] = static_cast<D>(v.x);
-        dst[off(2 * i + 1, j)] = static_cast<D>(v.y);
-      }
-    }
+    put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, tile[jj][ii]);
   }
 }
 
