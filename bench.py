@@ -210,6 +210,14 @@ class ClockSampler:
                  "-lms", os.environ.get("MDGEMM_BENCH_CLOCK_MS", "1000")], stdout=self.file, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        self.device_index = device_index
+        # the first sample lands before the timed region starts (a region of a few ms -- cfg1 --
+        # would otherwise end before nvidia-smi has started: no clock record at all)
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < 5.0:
+            if os.path.getsize(self.file.name) > 0:
+                break
+            time.sleep(0.01)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -223,6 +231,16 @@ class ClockSampler:
             if len(parts) >= 8:
                 rows.append(parts)
         os.unlink(self.file.name)
+        if len(rows) < 2:  # a short region: one more sample right at its end, so two bracket it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device_index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                for line in out.stdout.splitlines():
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 8:
+                        rows.append(parts)
+            except (OSError, subprocess.SubprocessError):
+                pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]

@@ -23,6 +23,28 @@
 
 #include "desc.h"
 
+// Device-side checks of the checked build (make -C paper_1901_06015_b200/csrc
+// checked -> libmdgemm_b200_checked.so, loaded with MDGEMM_LIBRARY=checked):
+// every index the kernels derive -- tile and k-block of a TMA source, shared
+// memory destination of a bulk copy, stream-K slot, packed-buffer offset, C
+// element of the element-wise epilogues -- is checked against its bound, and
+// a violation traps with a message.  The release build compiles them out.
+#ifdef MDG_DEVICE_CHECKS
+#include <cstdio>
+#define MDG_CHECK(cond, what)                                                                                  \
+  do {                                                                                                        \
+    if (!(cond)) {                                                                                            \
+      printf("mdgemm device check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__,         \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                                    \
+      __trap();                                                                                               \
+    }                                                                                                         \
+  } while (0)
+#else
+#define MDG_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+#endif
+
 namespace mdg {
 
 __device__ __forceinline__ double rnd(double v, bool single) {
@@ -269,6 +291,17 @@ __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
 
 // One TMA bulk copy global -> shared, completing on `bar` (tx bytes).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#ifdef MDG_DEVICE_CHECKS
+  {
+    extern __shared__ __align__(128) unsigned char mdg_dyn_smem[];
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const uint32_t lo = smem_u32(mdg_dyn_smem), d = smem_u32(dst);
+    MDG_CHECK(d >= lo && d + bytes <= lo + dyn, "bulk copy destination outside the dynamic shared memory");
+    MDG_CHECK((d & 15) == 0 && (bytes & 15) == 0 && (reinterpret_cast<uint64_t>(src) & 15) == 0,
+              "bulk copy not 16-byte aligned");
+  }
+#endif
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
           smem_u32(dst)),
@@ -450,6 +483,7 @@ __device__ __forceinline__ void fast_epilogue(unsigned char* smem, uint32_t regi
       const int oi = idx % orows, oj = idx / orows;
       const int64_t gi = oi0 + oi, gj = oj0 + oj;
       if (gi >= om || gj >= on) continue;
+      MDG_CHECK(gi >= 0 && gj >= 0 && gi < e.out.m && gj < e.out.n, "epilogue element outside C");
       R* cp = out + (gi * e.out.rs + gj * e.out.cs) * NC;
       R cv[NC];
       const R* tp = reinterpret_cast<const R*>(tbuf) + static_cast<size_t>(sidx(oi, oj)) * NC;
@@ -630,6 +664,11 @@ __device__ __forceinline__ Seg sched_seg(const Sched& s, const GemmDesc& d, int 
   }
   if (idx < s.start_tile - s.full0) return Seg{s.full0 + idx, 0, s.nk, SEG_FULL};
   return Seg{s.end_tile, s.end_k0, s.nk, SEG_END};
+}
+
+// Stream-K partial slot / publish flag b of a grid with G slots.
+__device__ __forceinline__ void check_sk_slot(int b, int64_t G) {
+  MDG_CHECK(b >= 0 && b < G, "stream-K slot out of range");
 }
 
 __device__ __forceinline__ void flag_release(int* f) {

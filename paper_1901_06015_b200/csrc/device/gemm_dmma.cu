@@ -90,6 +90,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
         if (after_epilogue) mbar_wait(segdone, (epis++) & 1);  // the epilogue reused the ring's memory
         int tm, tn;
         tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        MDG_CHECK(tm >= 0 && tm < tiles_m && tn >= 0 && tn < tiles_n && sg.k0 >= 0 && sg.k0 <= sg.k1 &&
+                      static_cast<int64_t>(sg.k1) * C::BK <= lpad,
+                  "producer tile / k-block range");
         const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
         const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
         for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
     double acc[C::MT][C::NT][2];
     if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
       const int prev = sc.sk - 1;
+      check_sk_slot(prev, d.sk_grid);
       if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
       named_sync(1, C::NCT);
       const double* slot = static_cast<const double*>(d.sk_partials) + static_cast<int64_t>(prev) * (C::BM * C::BN);
@@ -175,6 +179,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_dmma_kernel(const __
 
     if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
       const int self = sc.sk;
+      check_sk_slot(self, d.sk_grid);
       double* slot = static_cast<double*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN);
 #pragma unroll
       for (int i = 0; i < C::MT; ++i)

@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
       const Seg sg = ws_seg(sc, si);
       int tm, tn;
       tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+      MDG_CHECK(tm >= 0 && tm < tiles_m && tn >= 0 && tn < tiles_n && sg.k0 >= 0 && sg.k0 <= sg.k1 &&
+                    static_cast<int64_t>(sg.k1) * WS_BK <= lpad,
+                "producer tile / k-block range");
       const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * WS_BM * lpad;
       const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * WS_BN * lpad;
       for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
     const Seg sg = ws_seg(sc, si);
     double acc[WS_MT][WS_NT][2];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      check_sk_slot(sc.b - 1, d.sk_grid);
       if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, WS_MMA_THREADS);
       const double* slot =
@@ -325,6 +329,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) gemm_dmma_ws_kernel(const __gri
           for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
       __threadfence();
       named_sync(1, WS_MMA_THREADS);
+      check_sk_slot(sc.b, d.sk_grid);
       if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }
@@ -488,6 +493,9 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
         const Seg sg = ws_seg(sc, si);
         int tm, tn;
         tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        MDG_CHECK(tm >= 0 && tm < tiles_m && tn >= 0 && tn < tiles_n && sg.k0 >= 0 && sg.k0 <= sg.k1 &&
+                      static_cast<int64_t>(sg.k1) * WS_BK <= lpad,
+                  "producer tile / k-block range");
         const double* Ag = static_cast<const double*>(d.a.data) + static_cast<int64_t>(tm) * WS_BM * lpad;
         const double* Bg = static_cast<const double*>(d.b.data) + static_cast<int64_t>(tn) * WS_BN * lpad;
         for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
@@ -603,6 +611,7 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
     const Seg sg = ws_seg(sc, si);
     double acc[WS_MT][WS_NT][2];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      check_sk_slot(sc.b - 1, d.sk_grid);
       if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, WS_MMA_THREADS);
       const double* slot =
@@ -651,6 +660,7 @@ __global__ void __launch_bounds__(WE_THREADS, 1) gemm_dmma_ws_epi_kernel(const _
           for (int h = 0; h < 2; ++h) __stcg(slot + ((i * WS_NT + j) * 2 + h) * WS_MMA_THREADS + tid, acc[i][j][h]);
       __threadfence();
       named_sync(1, WS_MMA_THREADS);
+      check_sk_slot(sc.b, d.sk_grid);
       if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }

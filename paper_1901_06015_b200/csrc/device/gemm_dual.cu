@@ -107,6 +107,7 @@ __device__ __forceinline__ int job_of(const DualJob* jobs, int njobs, int v) {
 template <int CDT>
 __device__ __forceinline__ typename OutType<CDT>::R* c_ptr(const DView& o, int64_t oi, int64_t oj) {
   using O = OutType<CDT>;
+  MDG_CHECK(oi >= 0 && oj >= 0 && oi < o.m && oj < o.n, "dual epilogue element outside C");
   return reinterpret_cast<typename O::R*>(o.base) + (oi * o.rs + oj * o.cs) * O::NC;
 }
 
@@ -358,6 +359,8 @@ __device__ __forceinline__ void dual_body(const DualDesc& d) {
         const DualJob& jb = jobs[job_of(jobs, njobs, v)];
         int tm, tn;
         tile_coords(jb.tile_begin + v - jb.tile0, jb.tiles_m, jb.tiles_n, 0, tm, tn);
+        MDG_CHECK(v >= jb.tile0 && tm >= 0 && tm < jb.tiles_m && tn >= 0 && tn < jb.tiles_n && jb.lpad % BK == 0,
+                  "dual producer job / tile");
         if (d.prefetch_c) prefetch_c(jb, tm, tn, BM, BN);
         // panels of SA / BK (SB / BK) elements per line
         const T* Ag = static_cast<const T*>(jb.a) + static_cast<int64_t>(tm) * (SA / BK) * jb.lpad;

@@ -81,6 +81,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
         if (after_epilogue) mbar_wait(segdone, (epis++) & 1);  // the epilogue reused the ring's memory
         int tm, tn;
         tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+        MDG_CHECK(tm >= 0 && tm < tiles_m && tn >= 0 && tn < tiles_n && sg.k0 >= 0 && sg.k0 <= sg.k1 &&
+                      static_cast<int64_t>(sg.k1) * C::BK <= lpad,
+                  "producer tile / k-block range");
         const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * C::BM * lpad;
         const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * C::BN * lpad;
         for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
@@ -123,6 +126,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
     uint64_t acc[8][4];
     if (SK && sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
       const int prev = sc.sk - 1;
+      check_sk_slot(prev, d.sk_grid);
       if (tid == 0) flag_acquire_wait(d.sk_flags + prev);
       named_sync(1, C::NCT);
       const uint64_t* slot =
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) gemm_ffma_kernel(const __
 
     if (SK && sg.kind == SEG_START) {  // publish the first k-blocks of the tile for CTA b+1
       const int self = sc.sk;
+      check_sk_slot(self, d.sk_grid);
       uint64_t* slot = static_cast<uint64_t*>(d.sk_partials) + static_cast<int64_t>(self) * (C::BM * C::BN / 2);
 #pragma unroll
       for (int i = 0; i < 8; ++i)

@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
       const Seg sg = fw_seg(sc, si);
       int tm, tn;
       tile_coords(sg.tile, tiles_m, tiles_n, d.group_rows, tm, tn);
+      MDG_CHECK(tm >= 0 && tm < tiles_m && tn >= 0 && tn < tiles_n && sg.k0 >= 0 && sg.k0 <= sg.k1 &&
+                    static_cast<int64_t>(sg.k1) * FW_BK <= lpad,
+                "producer tile / k-block range");
       const float* Ag = static_cast<const float*>(d.a.data) + static_cast<int64_t>(tm) * FW_BM * lpad;
       const float* Bg = static_cast<const float*>(d.b.data) + static_cast<int64_t>(tn) * FW_BN * lpad;
       for (int kb = sg.k0; kb < sg.k1; ++kb, ++it) {
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
     const Seg sg = fw_seg(sc, si);
     uint64_t acc[8][4];
     if (sg.kind == SEG_END) {  // continue CTA b-1's accumulation of this tile
+      check_sk_slot(sc.b - 1, d.sk_grid);
       if (tid == 0) flag_acquire_wait(d.sk_flags + sc.b - 1);
       named_sync(1, FW_MMA_THREADS);
       const uint64_t* slot =
@@ -260,6 +264,7 @@ __global__ void __launch_bounds__(FW_THREADS, 1) gemm_ffma_ws_kernel(const __gri
         for (int p = 0; p < 4; ++p) __stcg(slot + (i * 4 + p) * FW_MMA_THREADS + tid, acc[i][p]);
       __threadfence();
       named_sync(1, FW_MMA_THREADS);
+      check_sk_slot(sc.b, d.sk_grid);
       if (tid == 0) flag_release(d.sk_flags + sc.b);
       continue;
     }

@@ -63,8 +63,9 @@ __device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ ds
   const int sh = d.pd_shift;
   auto off = [&](int64_t pr, int64_t pc) -> int64_t {
     const int64_t x = SIDE == MDG_SIDE_LEFT ? pr : pc, y = SIDE == MDG_SIDE_LEFT ? pc : pr;
-    if (sh >= 0) return ((x >> sh) * LP + y) * PT + (x & (PD - 1));
-    return (x / PD) * PT * LP + y * PT + x % PD;
+    const int64_t o = sh >= 0 ? ((x >> sh) * LP + y) * PT + (x & (PD - 1)) : (x / PD) * PT * LP + y * PT + x % PD;
+    MDG_CHECK(o >= 0 && o < d.panels * LP * PT && y < LP, "packed offset outside the panels");
+    return o;
   };
   if constexpr (FMT == MDG_FMT_STANDARD) {
     if constexpr (SRC_COMPLEX) {
