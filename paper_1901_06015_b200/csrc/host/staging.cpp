@@ -1129,6 +1129,23 @@ void gemm_batch_async(const std::vector<GemmCall>& calls, const Config& cfg, voi
 
 void gemm(Scalar alpha, const MatrixView& a, const MatrixView& b, Scalar beta, const MatrixView& c,
           const Config& cfg, FlopCounter* fc) {
+  // A lone call on device operands: plan it and run it on the legacy stream,
+  // then synchronise -- what the batch runner does for one such call, without
+  // its copy streams, fork / join events and stream arenas (the same kernels
+  // and workspace sizes, so the same bits).  MDGEMM_LONE_FASTPATH=0: always the
+  // batch runner.
+  static const bool fast = [] {
+    const char* f = std::getenv("MDGEMM_LONE_FASTPATH");
+    return !(f && std::atoi(f) == 0);
+  }();
+  auto on_device = [](const MatrixView& v) { return v.m == 0 || v.n == 0 || is_device_ptr(v.base); };
+  if (fast && on_device(c) && on_device(a) && on_device(b)) {
+    if (ranges_overlap(c, a) || ranges_overlap(c, b)) throw Error("gemm: C must not alias A or B");
+    const ExecutionPlan p = plan(alpha, a, b, beta, c, cfg);
+    execute(p, cfg.numerics, cudaStreamLegacy, fc, cfg.splitk);
+    cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "gemm synchronisation");
+    return;
+  }
   gemm_batch({GemmCall{alpha, a, b, beta, c}}, cfg, fc);
 }
 
