@@ -112,14 +112,24 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
   const bool i_fast = d.src.rs <= d.src.cs;
 
   if (i_fast == (SIDE == MDG_SIDE_LEFT)) {  // no transpose (uniform per launch)
+    // all of the thread's loads in flight before the first store
+    double2 raw[TILE / ROWS];
+#pragma unroll
+    for (int r = 0; r < TILE / ROWS; ++r) {
+      const int ii = i_fast ? lane : row + ROWS * r;
+      const int jj = i_fast ? row + ROWS * r : lane;
+      const int64_t i = i0 + ii, j = j0 + jj;
+      raw[r] = make_double2(0.0, 0.0);
+      if (i < d.src.m && j < d.src.n) raw[r] = load_src<S, SRC_COMPLEX>(d.src, i, j);
+    }
 #pragma unroll
     for (int r = 0; r < TILE / ROWS; ++r) {
       const int ii = i_fast ? lane : row + ROWS * r;
       const int jj = i_fast ? row + ROWS * r : lane;
       const int64_t i = i0 + ii, j = j0 + jj;
       if (i >= d.ext_i || j >= d.ext_j) continue;
-      double2 v = make_double2(0.0, 0.0);  // padded slots take literal zeros
-      if (i < d.src.m && j < d.src.n) v = process(load_src<S, SRC_COMPLEX>(d.src, i, j), d);
+      // padded slots take literal zeros (not processed: the reference pads with +0 / -0 as stored)
+      const double2 v = (i < d.src.m && j < d.src.n) ? process(raw[r], d) : make_double2(0.0, 0.0);
       put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, v);
     }
     return;

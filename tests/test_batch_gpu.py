@@ -186,3 +186,22 @@ def test_batch_eviction_chain(monkeypatch):
                  cfg)
     for i in range(8):
         assert mats[i].buf.tobytes() == ref[i].buf.tobytes(), i
+
+
+@pytest.mark.parametrize("label,shape", [("dssd", (1024, 1024, 1024)), ("zzzd", (300, 257, 333)),
+                                         ("cdds", (130, 700, 2100)), ("sddd", (2048, 2048, 64)),
+                                         ("szzs", (64, 64, 8))])
+def test_lone_device_call_equals_the_batch_runner(label, shape):
+    # gemm() on device operands takes the lone-call path (plan -> execute on the legacy stream); a
+    # one-call gemm_batch goes through the batch runner.  Same kernels, same bits, same flop count.
+    m, n, k = shape
+    p = Problem(label, m, n, k, seed=17)
+    cfg = config({"gpu.numerics": "fast"})
+    dA, dB, dC = p.device()
+    da, db, dc = p.views(A=dA, B=dB, C=dC)
+    f1 = M.gemm(SCALARS["p7"], da, db, SCALARS["cfg2_beta"], dc, cfg)
+    eA, eB, eC = p.device()
+    ea, eb, ec = p.views(A=eA, B=eB, C=eC)
+    f2 = M.gemm_batch([(SCALARS["p7"], ea, eb, SCALARS["cfg2_beta"], ec)], cfg)
+    assert f1 == f2
+    assert dC.bytes().tobytes() == eC.bytes().tobytes()

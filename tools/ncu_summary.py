@@ -2,7 +2,7 @@
 a markdown table of the key metrics per kernel and profiles/ncu_traffic.json
 (DRAM bytes per captured launch next to the algorithmic bytes).
 
-    python tools/ncu_summary.py gpurun_out/prof profiles/r01
+    python tools/ncu_summary.py gpurun_out/prof profiles/r01 [label]
 """
 import csv
 import json
@@ -51,8 +51,9 @@ def load(path):
 
 def main():
     src, dst = sys.argv[1], sys.argv[2]
+    label = sys.argv[3] if len(sys.argv) > 3 else "round 1 (tools/profile_r01.sh"
     os.makedirs(dst, exist_ok=True)
-    lines = ["# ncu --set full captures, round 1 (tools/profile_r01.sh, one launch each, --clock-control none)", "",
+    lines = [f"# ncu --set full captures, {label}, one launch each, --clock-control none)", "",
              "Launches: DMMA = `zzzd` 4096 (1m: me=8192, ne=4096, ke=8192), FFMA = `cccs` 4096 (same real dims), "
              "pack = the 1e pack of `zzzd`'s A, dmma_ws = the warp-specialised DMMA kernel on a lone `dddd` 4096 call, "
              "dmma_ws_epi = its epilogue-warp variant on cfg5 k=64 (`sddd` 32768^2 x 64), dual = one gemm_dual launch of "

@@ -105,48 +105,6 @@ __global__ void k_dmma_1684(double* out) {
   if (r == 1234.5) out[0] = r;
 }
 
-// m16n8k8: A 4, B 2, C 4.
-__global__ void k_dmma_1688(double* out) {
-  double a0 = threadIdx.x * 1e-3, a1 = 0.25, a2 = 0.125, a3 = 0.3, b0 = 0.5, b1 = 0.7;
-  double c[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
-  for (int it = 0; it < ITERS / 8; ++it) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
-                   : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
-  }
-  double r = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1] + c[i][2] + c[i][3];
-  if (r == 1234.5) out[0] = r;
-}
-
-// m16n8k16: A 8, B 4, C 4.
-__global__ void k_dmma_16816(double* out) {
-  double a[8], b[4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) b[i] = 0.5 + i;
-  double c[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) c[i][0] = c[i][1] = c[i][2] = c[i][3] = 0;
-  for (int it = 0; it < ITERS / 16; ++it) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
-                   : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
-                   : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
-                     "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
-  }
-  double r = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) r += c[i][0] + c[i][1] + c[i][2] + c[i][3];
-  if (r == 1234.5) out[0] = r;
-}
 
 template <typename F>
 static float time_it(F launch, int reps) {
@@ -266,10 +224,6 @@ int main(int argc, char** argv) {
     printf(", \"dmma884_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 4) * 8 * (8 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
     ms = time_it([&] { k_dmma_1684<<<grid, block>>>(dout); }, reps);
     printf(", \"dmma1684_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 4) * 4 * (16 * 8 * 4 * 2) / (ms * 1e-3) / 1e12);
-    ms = time_it([&] { k_dmma_1688<<<grid, block>>>(dout); }, reps);
-    printf(", \"dmma1688_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 8) * 4 * (16 * 8 * 8 * 2) / (ms * 1e-3) / 1e12);
-    ms = time_it([&] { k_dmma_16816<<<grid, block>>>(dout); }, reps);
-    printf(", \"dmma16816_w%d_tflops\": %.3f", wpb, nwarps * (ITERS / 16) * 4 * (16 * 8 * 16 * 2) / (ms * 1e-3) / 1e12);
   }
   CK(cudaGetLastError());
   printf("}\n");
