@@ -799,16 +799,16 @@ void dual_launch(const mdg::DualDesc& desc, double flops_d, double flops_f, cuda
   }();
   d.sleep_ns = sleep_ns;
   prof::Scope scope(MDG_KERNEL_DUAL_D, st, flops_d, MDG_KERNEL_DUAL_F, flops_f);
-  // One SM is left to the next launch's pack kernels: a dual CTA holds every
-  // register of its SM, so without it those packs wait for the launch to
-  // drain and the kernel stream idles while they run.  Measured on the cfg2
-  // sweep (profiles/r02/dual_spare_sms.txt): 0 -> 52,470 GFLOPS, 1 -> 52,640,
-  // 2 -> 52,620, 4 -> 52,390 (the packs of a launch overlap the current one
-  // on the spare SMs; the dual launch loses 1/148 of its SMs).
-  // MDGEMM_DUAL_SPARE_SMS overrides.
+  // Two SMs are left to the next launches' pack kernels: a dual CTA holds
+  // every register of its SM, so without them those packs wait for the launch
+  // to drain and the kernel stream idles while they run.  Measured on the cfg2
+  // sweep (profiles/r02/dual_spare_sms.txt): 0 spare SMs -> 52,470 GFLOPS,
+  // 1 -> 52,640, 2 -> 52,620, 4 -> 52,390 with two pack arenas; 2 spare SMs
+  // with three arenas (staging.cpp: dual_arenas, the packs may run two
+  // launches ahead) -> 52,710.  MDGEMM_DUAL_SPARE_SMS overrides.
   static const int spare = [] {
     const char* f = std::getenv("MDGEMM_DUAL_SPARE_SMS");
-    return f ? std::max(0, std::atoi(f)) : 1;
+    return f ? std::max(0, std::atoi(f)) : 2;
   }();
   cuda_check(mdg::launch_gemm_dual(d, std::max(1, device_sms() - spare), st), "dual-pipe gemm kernel");
 }

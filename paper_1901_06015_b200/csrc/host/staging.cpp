@@ -212,6 +212,16 @@ struct Unit {
   size_t bytes = 0;         // packed operand bytes of the dual jobs
 };
 
+constexpr int kMaxDualArenas = 4;
+int dual_arenas() {  // MDGEMM_DUAL_ARENAS: packed-operand arenas of a dual batch (2..4)
+  static const int n = [] {
+    const char* f = std::getenv("MDGEMM_DUAL_ARENAS");
+    const int v = f ? std::atoi(f) : 3;
+    return std::min(kMaxDualArenas, std::max(2, v));
+  }();
+  return n;
+}
+
 int dual_mode() {
   const char* f = std::getenv("MDGEMM_DUAL");  // 0 off, 1 auto, 2 force (even one-precision batches)
   return f ? std::atoi(f) : 1;
@@ -514,7 +524,11 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
     return events.back();
   };
   std::vector<std::pair<Window, std::byte*>> residents;  // host window -> device copy
-  void* arena[2] = {nullptr, nullptr};
+  // Packed-operand arenas, used round robin by the launches: the packs of
+  // launch u go into arena u % n once launch u - n is done with it, so they may
+  // run that many launches ahead (on the SMs a dual launch leaves free).
+  void* arena[kMaxDualArenas] = {};
+  const int narenas = dual_arenas();
   int* counters = nullptr;
   bool failed = true;
   auto cleanup = [&](bool wait) {
@@ -595,7 +609,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
     };
     for (size_t i = 0; i < n; ++i) rebase(i);
     if (arena_bytes > 0)
-      for (void*& a : arena) cuda_check(ws_alloc(&a, arena_bytes, P), "workspace allocation");
+      for (int a = 0; a < narenas; ++a) cuda_check(ws_alloc(&arena[a], arena_bytes, P), "workspace allocation");
     // per-launch tile counters of the dynamic tile order (MDGEMM_DUAL_DYNAMIC=1; the
     // default static boustrophedon order measured 0.7 % faster on the cfg2 sweep: the
     // atomic fetch at every tile start delays the producer's first copies)
@@ -629,7 +643,8 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
         execute_scheduled(c.plan, cfg.numerics, K, fc, true, nullptr, 0, nullptr, cfg.splitk);
       } else {
         // packs: after the kernel that last used this arena and after writers of the A/B read
-        if (ui >= 2 && k_done[ui - 2]) cuda_check(cudaStreamWaitEvent(P, k_done[ui - 2], 0), "arena reuse");
+        if (ui >= static_cast<size_t>(narenas) && k_done[ui - narenas])
+          cuda_check(cudaStreamWaitEvent(P, k_done[ui - narenas], 0), "arena reuse");
         long abw = -1;
         for (size_t i : members)
           if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
@@ -642,7 +657,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
         int npk = 0;
         mdg::DualDesc dd{};
         double flops_d = 0, flops_f = 0;
-        char* w = static_cast<char*>(arena[ui % 2]);
+        char* w = static_cast<char*>(arena[ui % narenas]);
         size_t off = 0;
         for (int grp = 0; grp < 2; ++grp) {
           const std::vector<Piece>& lst = grp == 0 ? u.d : u.f;
@@ -771,7 +786,7 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S, cu
                   FlopCounter* fc) {
   DualPlan plan;
   if (!dual_schedule(cs, cfg, plan)) return false;
-  const size_t budget = reserve_for_batch(plan.host_bytes, plan.arena_bytes, 2);
+  const size_t budget = reserve_for_batch(plan.host_bytes, plan.arena_bytes, dual_arenas());
   if (plan.host_bytes > budget) {  // does not fit: the stream scheduler evicts as it goes
     for (Call& c : cs) c.dev_read[0] = c.dev_read[1] = c.dev_write = Window{};
     return false;
