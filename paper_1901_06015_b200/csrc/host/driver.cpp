@@ -786,6 +786,24 @@ void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* 
   job->tiles_n = static_cast<int32_t>((p.n + bn - 1) / bn);
 }
 
+int dual_grid() {
+  // Two SMs are left to the next launches' pack kernels: a dual CTA holds
+  // every register of its SM, so without them those packs wait for the launch
+  // to drain and the kernel stream idles while they run.  Measured on the cfg2
+  // sweep (profiles/r02/dual_spare_sms.txt): 0 spare SMs -> 52,470 GFLOPS,
+  // 1 -> 52,640, 2 -> 52,620, 4 -> 52,390 with two pack arenas; 2 spare SMs
+  // with three arenas (staging.cpp: dual_arenas, the packs may run two
+  // launches ahead) -> 52,710.  MDGEMM_DUAL_SPARE_SMS overrides.
+  static const int spare = [] {
+    const char* f = std::getenv("MDGEMM_DUAL_SPARE_SMS");
+    return f ? std::max(0, std::atoi(f)) : 2;
+  }();
+  int dev_count = 0;
+  const int sms = cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 ? device_sms() : 148;
+  cudaGetLastError();
+  return std::max(1, sms - spare);
+}
+
 void dual_launch(const mdg::DualDesc& desc, double flops_d, double flops_f, cudaStream_t st) {
   mdg::DualDesc& d = const_cast<mdg::DualDesc&>(desc);
   static const int prefetch = [] {  // tuning: MDGEMM_DUAL_PREFETCH = 0 turns the C L2 prefetch off
@@ -799,18 +817,7 @@ void dual_launch(const mdg::DualDesc& desc, double flops_d, double flops_f, cuda
   }();
   d.sleep_ns = sleep_ns;
   prof::Scope scope(MDG_KERNEL_DUAL_D, st, flops_d, MDG_KERNEL_DUAL_F, flops_f);
-  // Two SMs are left to the next launches' pack kernels: a dual CTA holds
-  // every register of its SM, so without them those packs wait for the launch
-  // to drain and the kernel stream idles while they run.  Measured on the cfg2
-  // sweep (profiles/r02/dual_spare_sms.txt): 0 spare SMs -> 52,470 GFLOPS,
-  // 1 -> 52,640, 2 -> 52,620, 4 -> 52,390 with two pack arenas; 2 spare SMs
-  // with three arenas (staging.cpp: dual_arenas, the packs may run two
-  // launches ahead) -> 52,710.  MDGEMM_DUAL_SPARE_SMS overrides.
-  static const int spare = [] {
-    const char* f = std::getenv("MDGEMM_DUAL_SPARE_SMS");
-    return f ? std::max(0, std::atoi(f)) : 2;
-  }();
-  cuda_check(mdg::launch_gemm_dual(d, std::max(1, device_sms() - spare), st), "dual-pipe gemm kernel");
+  cuda_check(mdg::launch_gemm_dual(d, dual_grid(), st), "dual-pipe gemm kernel");
 }
 
 }  // namespace mdgemm

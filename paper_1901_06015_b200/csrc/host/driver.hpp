@@ -102,8 +102,11 @@ DualPrep dual_prepare(const ExecutionPlan& p);
 // Launch the two pack kernels into ws (stream-ordered) and describe the job
 // (p's views must be the device views the kernels read).
 void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job);
-// One dual launch over d's job lists (grid = SMs); flops per group for the
-// profiling hook.
+// CTAs of a dual launch: the SMs less the ones left to the packs (148 B200
+// SMs when no device is visible: the host-only schedule).
+int dual_grid();
+// One dual launch over d's job lists (grid = dual_grid()); flops per group for
+// the profiling hook.
 void dual_launch(const mdg::DualDesc& d, double flops_d, double flops_f, cudaStream_t st);
 
 // The dual-pipe batch schedule of gemm_batch (host only, no device work): one
