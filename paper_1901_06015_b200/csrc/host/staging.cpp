@@ -186,8 +186,9 @@ size_t reserve_for_batch(size_t host_bytes, size_t arena_bytes, int nstreams) {
 // durations match, so both pipes of every SM work at once.  A launch holds
 // only calls whose dependencies (device-memory conflicts, as in the stream
 // scheduler) completed in earlier launches; launches run in order on one
-// stream, their packs on a second stream into two alternating arenas (the
-// packs of launch u+1 fill SMs freed by the tail of launch u).  Calls the
+// stream, their packs on other streams into rotating arenas (dual_arenas,
+// three by default: the packs run up to two launches ahead, on the SMs each
+// launch leaves free -- driver.cpp: dual_grid).  Calls the
 // kernel does not take (EXACT numerics, k = 0, ...) run in the same order
 // through execute().  Host operands are staged once up front (only when no
 // two host windows of the batch partially overlap and they fit the resident
