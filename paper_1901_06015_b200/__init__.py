@@ -27,8 +27,10 @@ __all__ = [
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # MDGEMM_LIBRARY=checked loads the build with device-side index checks
 # (make -C paper_1901_06015_b200/csrc checked; tests only)
-_LIB_PATH = os.path.join(_HERE, "libmdgemm_b200_checked.so" if os.environ.get("MDGEMM_LIBRARY") == "checked"
-                         else "libmdgemm_b200.so")
+# (or the path of another build of the library: A/B experiments)
+_LIB_ENV = os.environ.get("MDGEMM_LIBRARY", "")
+_LIB_PATH = (os.path.join(_HERE, "libmdgemm_b200_checked.so") if _LIB_ENV == "checked"
+             else _LIB_ENV if _LIB_ENV.endswith(".so") else os.path.join(_HERE, "libmdgemm_b200.so"))
 
 # enumerations (mdgemm_b200.h)
 DT_S, DT_D, DT_C, DT_Z = 0, 1, 2, 3

@@ -13,11 +13,25 @@
 namespace mdg {
 namespace {
 
-constexpr int TILE = packtile::TILE;
 constexpr int PACK_THREADS = 256;
+// CTAs per SM the register budget must allow (__launch_bounds__ minimum):
+// the tile loads are latency-bound, and unbounded ptxas picks 48-60 registers,
+// four 256-thread CTAs per SM (a 2048^2 pack pair: 46 % achieved occupancy,
+// 2.2 TB/s).  Real sources at six per SM (<= 40 registers): dddd 2048 pack
+// 44 -> 40 us, 4096 159 -> 135 us, dssd 1024 13.7 -> 12.7 us; complex sources
+// (1e / 1r, more live values) stay unbounded -- bounded they spill and run
+// slower (zzzd 4096 252 -> 258 us).  Cfg2 sweep +0.4 % (profiles/r02/pack_occupancy.txt).
+#ifndef MDG_PACK_MIN_BLOCKS_REAL
+#define MDG_PACK_MIN_BLOCKS_REAL 6
+#endif
+#ifndef MDG_PACK_MIN_BLOCKS_COMPLEX
+#define MDG_PACK_MIN_BLOCKS_COMPLEX 4
+#endif
+template <bool SRC_COMPLEX>
+constexpr int pack_min_blocks() { return SRC_COMPLEX ? MDG_PACK_MIN_BLOCKS_COMPLEX : MDG_PACK_MIN_BLOCKS_REAL; }
 
 template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE>
-__global__ void __launch_bounds__(PACK_THREADS) pack_kernel(PackDesc d, D* __restrict__ dst) {
+__global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>()) pack_kernel(PackDesc d, D* __restrict__ dst) {
   __shared__ packtile::Tile tile;
   packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS>(d, dst, blockIdx.x, tile, threadIdx.x,
                                                                    [] { __syncthreads(); });
@@ -27,7 +41,7 @@ __global__ void __launch_bounds__(PACK_THREADS) pack_kernel(PackDesc d, D* __res
 // precision and format (the side is decided per CTA): one launch instead of
 // two, and the two packs' tiles share the waves.
 template <typename S, bool SRC_COMPLEX, typename D, int FMT>
-__global__ void __launch_bounds__(PACK_THREADS)
+__global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
     pack_pair_kernel(const __grid_constant__ PackDesc d0, D* __restrict__ dst0, const __grid_constant__ PackDesc d1,
                      D* __restrict__ dst1, int64_t tiles0) {
   __shared__ packtile::Tile tile;
