@@ -159,8 +159,24 @@ struct DualDesc {
 static_assert(sizeof(DualDesc) <= 32000, "DualDesc exceeds the kernel parameter space");
 constexpr int DUAL_D_BM = 128, DUAL_D_BN = 128, DUAL_F_BM = 64, DUAL_F_BN = 128, DUAL_BK = 16, DUAL_F_BK = 32;
 
+// Many packs in one launch (pack.cu: pack_group_kernel): the packs of a dual
+// launch's FP64 or FP32 jobs -- up to both operands of DUAL_MAX_JOBS calls,
+// any mix of source type, target, format and side; CTA b packs tile b -
+// tile0[j] of pack j (tile0: prefix sums of the packs' tile counts).
+constexpr int PACK_GROUP_MAX = 2 * DUAL_MAX_JOBS;
+struct PackGroup {
+  int32_t n;
+  int32_t pad0;
+  int64_t tile0[PACK_GROUP_MAX + 1];
+  void* dst[PACK_GROUP_MAX];
+  PackDesc d[PACK_GROUP_MAX];
+};
+static_assert(sizeof(PackGroup) <= 32000, "PackGroup exceeds the kernel parameter space");
+
 // ---- host launchers (defined in the .cu files) ----
 cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s);
+// g.n packs in one launch (fills g.tile0[g.n]); their panel padding rows too.
+cudaError_t launch_pack_group(PackGroup& g, cudaStream_t s);
 // Both packs of a call in one launch; valid when pack_pair_ok (same source
 // type, target precision and format), else it falls back to two launches.
 cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s);

@@ -8,6 +8,8 @@
 // coalesced along the source's unit-stride axis and written coalesced along
 // the packed buffer's contiguous axis (rows for left panels, columns for
 // right panels), so a transposing pack costs one HBM read and one HBM write.
+#include <type_traits>
+
 #include "pack_tile.cuh"
 
 namespace mdg {
@@ -54,6 +56,61 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
     packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
   else
     packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+}
+
+// Packs of at least this many 32x32 tiles (a 1024^2 real operand) get their
+// own launch in launch_pack_group.
+constexpr int64_t kGroupLargeTiles = 1024;
+
+// One launch over many packs (PackGroup): CTA b finds its pack by binary
+// search over the tile prefix sums, then runs that pack's tile -- the kernel
+// instance for the pack's source type / target / format / side picked at run
+// time (uniform per CTA).  A dual launch's 20-70 small packs then cost one
+// launch instead of one or two each.
+template <typename S, bool SC, typename D>
+__device__ __forceinline__ void group_tile(const PackDesc& d, void* dst, int64_t bid, packtile::Tile& tile) {
+  auto sync = [] { __syncthreads(); };
+  auto side = [&](auto fmt) {
+    constexpr int FMT = decltype(fmt)::value;
+    if (d.side == MDG_SIDE_LEFT)
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_LEFT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+                                                                      sync);
+    else
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+                                                                       sync);
+  };
+  if constexpr (SC) {
+    if (d.format == MDG_FMT_ONEE) return side(std::integral_constant<int, MDG_FMT_ONEE>{});
+    if (d.format == MDG_FMT_ONER) return side(std::integral_constant<int, MDG_FMT_ONER>{});
+  }
+  side(std::integral_constant<int, MDG_FMT_STANDARD>{});
+}
+
+__global__ void __launch_bounds__(PACK_THREADS, 4) pack_group_kernel(const __grid_constant__ PackGroup g) {
+  __shared__ packtile::Tile tile;
+  __shared__ PackDesc sd;  // this CTA's pack: read once from the parameter space (26 KB: the
+                           // constant cache holds little of it), then from shared memory
+  const int64_t bid = blockIdx.x;
+  int lo = 0, hi = g.n - 1;  // the last pack whose first tile is <= bid
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (g.tile0[mid] <= bid) lo = mid;
+    else hi = mid - 1;
+  }
+  static_assert(sizeof(PackDesc) % 4 == 0, "PackDesc copied as words");
+  if (threadIdx.x < sizeof(PackDesc) / 4)
+    reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(&g.d[lo])[threadIdx.x];
+  __syncthreads();
+  const PackDesc& d = sd;
+  void* dst = g.dst[lo];
+  const int64_t t = bid - g.tile0[lo];
+  const bool ts = d.target_single != 0;
+  switch (d.src.dtype) {
+    case MDG_DT_S: ts ? group_tile<float, false, float>(d, dst, t, tile) : group_tile<float, false, double>(d, dst, t, tile); break;
+    case MDG_DT_D: ts ? group_tile<double, false, float>(d, dst, t, tile) : group_tile<double, false, double>(d, dst, t, tile); break;
+    case MDG_DT_C: ts ? group_tile<float, true, float>(d, dst, t, tile) : group_tile<float, true, double>(d, dst, t, tile); break;
+    default: ts ? group_tile<double, true, float>(d, dst, t, tile) : group_tile<double, true, double>(d, dst, t, tile); break;
+  }
 }
 
 template <typename S, bool SC, typename D, int FMT>
@@ -133,6 +190,37 @@ cudaError_t launch_pack(const PackDesc& d, void* dst, cudaStream_t s) {
   }
   if (e != cudaSuccess) return e;
   return pad(d, dst, s);
+}
+
+cudaError_t launch_pack_group(PackGroup& g, cudaStream_t s) {
+  if (g.n <= 0) return cudaSuccess;
+  if (g.n > PACK_GROUP_MAX) return cudaErrorInvalidValue;
+  // Large packs keep their own launch: the type-specialised kernels run at a
+  // higher occupancy than the run-time-dispatched one; the small ones (the
+  // launch latency dominates them) share one launch.
+  int keep = 0;
+  cudaError_t e = cudaSuccess;
+  for (int j = 0; j < g.n && e == cudaSuccess; ++j) {
+    if (packtile::pack_tiles(g.d[j]) >= kGroupLargeTiles) {
+      e = launch_pack(g.d[j], g.dst[j], s);
+    } else {
+      g.d[keep] = g.d[j];
+      g.dst[keep++] = g.dst[j];
+    }
+  }
+  if (e != cudaSuccess) return e;
+  g.n = keep;
+  int64_t tiles = 0;
+  for (int j = 0; j < g.n; ++j) {
+    g.tile0[j] = tiles;
+    tiles += packtile::pack_tiles(g.d[j]);
+  }
+  g.tile0[g.n] = tiles;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  if (tiles > 0) pack_group_kernel<<<static_cast<unsigned>(tiles), PACK_THREADS, 0, s>>>(g);
+  e = cudaGetLastError();
+  for (int j = 0; j < g.n && e == cudaSuccess; ++j) e = pad(g.d[j], g.dst[j], s);
+  return e;
 }
 
 cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {

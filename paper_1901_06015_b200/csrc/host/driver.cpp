@@ -755,22 +755,15 @@ DualPrep dual_prepare(const ExecutionPlan& p) {
   return d;
 }
 
-void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job) {
+void dual_describe(const ExecutionPlan& p, void* ws, mdg::DualJob* job, mdg::PackGroup* g, double* traffic) {
   const DualPrep d = dual_prepare(p);
   char* w = static_cast<char*>(ws);
-  if (mdg::pack_pair_ok(d.pa, d.pb)) {
-    prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a) + pack_traffic(p.b, d.bytes_b));
-    cuda_check(mdg::launch_pack_pair(d.pa, w, d.pb, w + d.off_b, st), "pack kernel");
-  } else {
-    {
-      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.a, d.bytes_a));
-      cuda_check(mdg::launch_pack(d.pa, w, st), "pack kernel");
-    }
-    {
-      prof::Scope scope(MDG_KERNEL_PACK, st, pack_traffic(p.b, d.bytes_b));
-      cuda_check(mdg::launch_pack(d.pb, w + d.off_b, st), "pack kernel");
-    }
-  }
+  if (g->n + 2 > mdg::PACK_GROUP_MAX) throw Error("dual_describe: pack group full");
+  g->d[g->n] = d.pa;
+  g->dst[g->n++] = w;
+  g->d[g->n] = d.pb;
+  g->dst[g->n++] = w + d.off_b;
+  if (traffic) *traffic += pack_traffic(p.a, d.bytes_a) + pack_traffic(p.b, d.bytes_b);
   const int64_t bm = d.single ? mdg::DUAL_F_BM : mdg::DUAL_D_BM;
   const int64_t bn = d.single ? mdg::DUAL_F_BN : mdg::DUAL_D_BN;
   *job = mdg::DualJob{};
@@ -784,6 +777,12 @@ void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* 
   job->pair = static_cast<int32_t>(p.pair_axis);
   job->tiles_m = static_cast<int32_t>((p.m + bm - 1) / bm);
   job->tiles_n = static_cast<int32_t>((p.n + bn - 1) / bn);
+}
+
+void dual_pack_group(mdg::PackGroup& g, double traffic, cudaStream_t st) {
+  if (g.n == 0) return;
+  prof::Scope scope(MDG_KERNEL_PACK, st, traffic);
+  cuda_check(mdg::launch_pack_group(g, st), "pack kernel");
 }
 
 int dual_grid() {

@@ -99,9 +99,11 @@ struct DualPrep {
   int32_t tiles = 0;        // tiles of the group's tile shape
 };
 DualPrep dual_prepare(const ExecutionPlan& p);
-// Launch the two pack kernels into ws (stream-ordered) and describe the job
-// (p's views must be the device views the kernels read).
-void dual_pack(const ExecutionPlan& p, void* ws, cudaStream_t st, mdg::DualJob* job);
+// Describe the job of p with its packed operands at ws and append the two
+// packs to g (p's views must be the device views the pack kernels read);
+// traffic += the packs' algorithmic bytes.  dual_pack_group launches g.
+void dual_describe(const ExecutionPlan& p, void* ws, mdg::DualJob* job, mdg::PackGroup* g, double* traffic);
+void dual_pack_group(mdg::PackGroup& g, double traffic, cudaStream_t st);
 // CTAs of a dual launch: the SMs less the ones left to the packs (148 B200
 // SMs when no device is visible: the host-only schedule).
 int dual_grid();

@@ -623,6 +623,7 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
       cuda_check(cudaMemsetAsync(counters, 0, units.size() * 2 * sizeof(int), K), "tile counters");
     }
     std::vector<cudaEvent_t> k_done(units.size(), nullptr);
+    std::vector<mdg::PackGroup> pack_groups(2);  // (26 KB each: kernel parameters of the group launches)
     const char* log_path = std::getenv("MDGEMM_DUAL_LOG");
     const bool log_units = log_path != nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> unit_ev(units.size(), {nullptr, nullptr});
@@ -651,11 +652,11 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
           if (ab_writer[i] >= 0) abw = std::max(abw, unit_of[static_cast<size_t>(ab_writer[i])]);
         if (abw >= 0 && k_done[static_cast<size_t>(abw)])
           cuda_check(cudaStreamWaitEvent(P, k_done[static_cast<size_t>(abw)], 0), "dependency");
-        // fan out: PX inherit P's dependencies, P joins them after the packs
+        // fan out: the FP32 jobs' packs on PX[0] (P's dependencies), P joins it;
+        // all packs of a group are one launch (pack_group_kernel)
         cudaEvent_t pgo = ev();
         cuda_check(cudaEventRecord(pgo, P), "event");
-        for (cudaStream_t q : PX) cuda_check(cudaStreamWaitEvent(q, pgo, 0), "fork");
-        int npk = 0;
+        cuda_check(cudaStreamWaitEvent(PX[0], pgo, 0), "fork");
         mdg::DualDesc dd{};
         double flops_d = 0, flops_f = 0;
         char* w = static_cast<char*>(arena[ui % narenas]);
@@ -663,11 +664,13 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
         for (int grp = 0; grp < 2; ++grp) {
           const std::vector<Piece>& lst = grp == 0 ? u.d : u.f;
           mdg::DualJob* jobs = grp == 0 ? dd.d : dd.f;
+          mdg::PackGroup& pg = pack_groups[grp];
+          pg.n = 0;
+          double traffic = 0;
           int32_t tiles = 0;
           for (size_t x = 0; x < lst.size(); ++x) {
             const size_t i = lst[x].call;
-            dual_pack(cs[i].plan, w + off, npk == 0 ? P : PX[npk - 1], &jobs[x]);
-            npk = (npk + 1) % 3;
+            dual_describe(cs[i].plan, w + off, &jobs[x], &pg, &traffic);
             off += prep[i].bytes;
             jobs[x].tile0 = tiles;
             jobs[x].tile_begin = lst[x].t0;
@@ -675,12 +678,13 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
             const ExecutionPlan& p = cs[i].plan;
             (grp == 0 ? flops_d : flops_f) += 2.0 * p.m * p.n * p.k * (lst[x].t1 - lst[x].t0) / prep[i].tiles;
           }
+          dual_pack_group(pg, traffic, grp == 0 ? P : PX[0]);
           (grp == 0 ? dd.nd : dd.nf) = static_cast<int32_t>(lst.size());
           (grp == 0 ? dd.tiles_d : dd.tiles_f) = tiles;
         }
-        for (cudaStream_t q : PX) {
+        {
           cudaEvent_t j = ev();
-          cuda_check(cudaEventRecord(j, q), "event");
+          cuda_check(cudaEventRecord(j, PX[0]), "event");
           cuda_check(cudaStreamWaitEvent(P, j, 0), "join");
         }
         cudaEvent_t packed = ev();
