@@ -43,9 +43,11 @@ def test_b200_arm_line():
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(roof) and roof["achieved"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["kind"] == "reference"
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
-    # 2 steps x 256 calls x 2 packs, plus the gemm launches: one dual-pipe launch per
-    # scheduled group of calls (mixed-precision batch), at most one (+ split-K reduce) per call
-    assert 2 * 256 * 2 < d["gpu_launches"] <= 2 * 256 * 4
+    # per step: one dual-pipe launch per scheduled group of calls, the packs of a group's small
+    # operands in one grouped launch (pack_group_kernel), large operands one launch each -- at
+    # least a pack and a gemm launch per group, at most 2 packs + gemm + split-K reduce per call
+    groups = d["step_kernels"]["dual_d"]["launches"]
+    assert 2 * 2 * groups <= d["gpu_launches"] <= 2 * 256 * 4
     assert d["step_kernels"]["dual_d"]["launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
 
