@@ -240,6 +240,10 @@ struct DualPlan {
   std::vector<Window> all;        // distinct host windows (each becomes one resident copy)
   size_t host_bytes = 0;
   size_t arena_bytes = 0;         // largest launch's packed operands
+  // estimated times (co-run rates): the longest dependency path through each call, the longest
+  // of all, and the larger of the two groups' total work (the span of a perfectly paired batch)
+  std::vector<double> through;
+  double critical = 0.0, span = 0.0;
 };
 
 }  // namespace
@@ -380,6 +384,21 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
     tail[i] = t + (kind[i] ? est[i] : 1e-5);
   }
   auto by_priority = [&](size_t x, size_t y) { return tail[x] != tail[y] ? tail[x] > tail[y] : x < y; };
+  {
+    std::vector<double> head(n, 0.0);  // longest path that ends where call i starts
+    double sum_d = 0, sum_f = 0;
+    for (size_t i = 0; i < n; ++i) {
+      const double e = kind[i] ? est[i] : 1e-5;
+      for (long s2 : succ[i]) head[static_cast<size_t>(s2)] = std::max(head[static_cast<size_t>(s2)], head[i] + e);
+      (kind[i] == 1 ? sum_d : sum_f) += kind[i] ? est[i] : 0.0;
+    }
+    P.through.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+      P.through[i] = head[i] + tail[i];
+      P.critical = std::max(P.critical, P.through[i]);
+    }
+    P.span = std::max(sum_d, sum_f);
+  }
   std::vector<Unit>& units = P.units;
   P.unit_of.assign(n, -1);
   P.first_unit.assign(n, -1);
@@ -787,10 +806,101 @@ void dual_emit(std::vector<Call>& cs, const Config& cfg, const Streams& S, const
   cleanup(failed);
 }
 
+// Long dependency chains.  Calls updating one C run one after another, and a
+// chain alternating FP64 and FP32 calls keeps one pipe idle whenever nothing
+// else is left to pair it with: when the batch's longest dependency path
+// exceeds kChainShare of its paired span, the calls on such paths are cut into
+// column panels (B and C column slices, the multi-GPU split of multi.cpp) --
+// independent sub-chains that the list scheduler pairs with each other.  Every
+// C element keeps its k order, so the bits do not change.  Device operands
+// with unit-stride C columns only (panels of other layouts share byte windows).
+constexpr double kChainShare = 0.25;
+constexpr int64_t kMinPanelColumns = 256, kPanelAlign = 128;
+constexpr int kMaxPanels = 8;
+
+int chain_split_mode() {  // MDGEMM_CHAIN_SPLIT: 0 off, 1 auto (default), 2..8 force that many panels
+  static const int v = [] {
+    const char* f = std::getenv("MDGEMM_CHAIN_SPLIT");
+    return f ? std::max(0, std::min(kMaxPanels, std::atoi(f))) : 1;
+  }();
+  return v;
+}
+
+MatrixView column_panel(const MatrixView& v, int64_t j0, int64_t nb) {
+  MatrixView out = v;
+  out.base = v.base + static_cast<size_t>(j0 * v.cs) * dtype_size(v.dtype);
+  out.n = nb;
+  return out;
+}
+
+// The batch with the calls on long paths cut into column panels; empty when
+// nothing is to be split.
+std::vector<GemmCall> split_long_chains(const std::vector<GemmCall>& calls, const DualPlan& plan) {
+  const int mode = chain_split_mode();
+  std::vector<GemmCall> out;
+  if (mode == 0 || plan.host_bytes != 0 || plan.span <= 0) return out;
+  const double limit = kChainShare * plan.span;
+  if (mode == 1 && plan.critical <= limit) return out;
+  const int panels = mode >= 2 ? mode : static_cast<int>(std::min<double>(kMaxPanels, std::ceil(plan.critical / limit)));
+  bool any = false;
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const GemmCall& g = calls[i];
+    const int64_t n = g.c.n;
+    const int pc = static_cast<int>(std::min<int64_t>(panels, n / kMinPanelColumns));
+    const bool cut = plan.kind[i] != 0 && g.c.rs == 1 && pc >= 2 && g.b.n == n &&
+                     (mode >= 2 || plan.through[i] > limit);
+    if (!cut) {
+      out.push_back(g);
+      continue;
+    }
+    any = true;
+    for (int r = 0; r < pc; ++r) {
+      int64_t j0 = 0, nb = 0;
+      shard_columns(n, pc, r, kPanelAlign, &j0, &nb);
+      if (nb == 0) continue;
+      out.push_back(GemmCall{g.alpha, g.a, column_panel(g.b, j0, nb), g.beta, column_panel(g.c, j0, nb)});
+    }
+  }
+  if (!any) out.clear();
+  return out;
+}
+
+// Estimated device time of a scheduled batch: per launch, the paired part of
+// its two groups at the co-run rates, what one group has beyond the other at
+// that group's rate alone (measured: FP64 31.5, FP32 50 TFLOP/s in the dual
+// kernel), and a fixed cost per launch (ramp-up, the last tiles' tail).
+double estimated_makespan(const DualPlan& plan) {
+  constexpr double kAloneD = 27.3 / 31.5, kAloneF = 30.7 / 50.0, kPerLaunch = 0.3e-3;
+  double t = 0;
+  for (const Unit& u : plan.units) {
+    if (u.classic >= 0) continue;
+    double td = 0, tf = 0;
+    for (const Piece& pc : u.d) td += plan.est[pc.call] * (pc.t1 - pc.t0) / plan.prep[pc.call].tiles;
+    for (const Piece& pc : u.f) tf += plan.est[pc.call] * (pc.t1 - pc.t0) / plan.prep[pc.call].tiles;
+    const double paired = std::min(td, tf);
+    t += paired + (td - paired) * kAloneD + (tf - paired) * kAloneF + kPerLaunch;
+  }
+  return t;
+}
+
+bool run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc,
+               const double* better_than = nullptr);
+
+// better_than: run only if the schedule's estimate beats this time (the finer batch of a caller
+// that has a schedule of its own); otherwise nothing is issued and the result is false.
 bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S, cudaStream_t user, bool sync,
-                  FlopCounter* fc) {
+                  FlopCounter* fc, const std::vector<GemmCall>& calls, const double* better_than) {
   DualPlan plan;
   if (!dual_schedule(cs, cfg, plan)) return false;
+  if (better_than) {
+    if (estimated_makespan(plan) >= *better_than) return false;
+  } else {
+    const std::vector<GemmCall> finer = split_long_chains(calls, plan);
+    if (!finer.empty()) {
+      const double mine = estimated_makespan(plan);
+      if (run_batch(finer, cfg, user, sync, fc, &mine)) return true;
+    }
+  }
   const size_t budget = reserve_for_batch(plan.host_bytes, plan.arena_bytes, dual_arenas());
   if (plan.host_bytes > budget) {  // does not fit: the stream scheduler evicts as it goes
     for (Call& c : cs) c.dev_read[0] = c.dev_read[1] = c.dev_write = Window{};
@@ -800,13 +910,19 @@ bool try_run_dual(std::vector<Call>& cs, const Config& cfg, const Streams& S, cu
   return true;
 }
 
-void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc) {
+bool run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream_t user, bool sync, FlopCounter* fc,
+               const double* better_than) {
   // Every plan first: policy and shape errors surface before any device work.
   std::vector<Call> cs(calls.size());
-  for (size_t i = 0; i < calls.size(); ++i) {
-    const GemmCall& g = calls[i];
-    if (ranges_overlap(g.c, g.a) || ranges_overlap(g.c, g.b)) throw Error("gemm: C must not alias A or B");
-    cs[i].plan = plan(g.alpha, g.a, g.b, g.beta, g.c, cfg);
+  try {
+    for (size_t i = 0; i < calls.size(); ++i) {
+      const GemmCall& g = calls[i];
+      if (ranges_overlap(g.c, g.a) || ranges_overlap(g.c, g.b)) throw Error("gemm: C must not alias A or B");
+      cs[i].plan = plan(g.alpha, g.a, g.b, g.beta, g.c, cfg);
+    }
+  } catch (const Error&) {
+    if (better_than) return false;  // a panel the planner rejects: the caller keeps its calls whole
+    throw;
   }
   // operand windows, and which live in host memory
   std::vector<Window> host_windows;
@@ -826,7 +942,8 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     }
   }
   const Streams S = device_streams();
-  if (try_run_dual(cs, cfg, S, user, sync, fc)) return;
+  if (try_run_dual(cs, cfg, S, user, sync, fc, calls, better_than)) return true;
+  if (better_than) return false;  // a finer batch that does not beat its caller's schedule
   static const int nstreams = [] {  // tuning: MDGEMM_STREAMS = 1..8 concurrent compute streams
     const char* f = std::getenv("MDGEMM_STREAMS");
     const int v = f ? std::atoi(f) : 4;  // default four concurrent streams
@@ -1088,6 +1205,7 @@ void run_batch(const std::vector<GemmCall>& calls, const Config& cfg, cudaStream
     throw;
   }
   cleanup(false);
+  return true;
 }
 
 }  // namespace

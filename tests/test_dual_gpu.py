@@ -214,3 +214,46 @@ def test_dual_many_small_calls(monkeypatch):
     assert ks["dual_d"]["launches"] >= 2, ks
     for p, w in zip(probs, want):
         assert p.C.buf.tobytes() == w.buf.tobytes(), p.label
+
+
+@pytest.mark.parametrize("shape", [(200, 1100, 96), (136, 1024, 40)])
+def test_long_chain_split_into_column_panels_equals_sequential_calls(monkeypatch, tmp_path, shape):
+    """A batch that is one long dependency chain (32 calls updating one device C, alternating
+    computation precisions) next to a short one: the calls on the long path are cut into column
+    panels (staging.cpp: split_long_chains) so that FP64 and FP32 panels of neighbouring calls pair
+    up.  Bits and FlopCounter must be those of the calls run one by one; a row-stored C is not cut."""
+    import re
+
+    import torch
+    monkeypatch.setenv("MDGEMM_DUAL", "1")
+    log = tmp_path / "dual.log"
+    monkeypatch.setenv("MDGEMM_DUAL_LOG", str(log))
+    cfg = config({"gpu.numerics": "fast"})
+    m, n, k = shape
+    long_labels = [l for l in LABELS if l[0] == "z"]
+    short_labels = [l for l in LABELS if l[0] == "s"][:6]
+    for c_kind, expect_split in (("col", True), ("row", False)):
+        log.write_text("")
+        probs = [Problem(l, m, n, k, seed=40 + i, trans_b=(i % 7 == 2), c_kind=c_kind) for i, l in enumerate(long_labels)]
+        probs += [Problem(l, 70, 130, 33, seed=90 + i) for i, l in enumerate(short_labels)]
+        shared = {"z": probs[0].C.clone(), "s": probs[len(long_labels)].C.clone()}
+        ref = {key: h.clone() for key, h in shared.items()}
+        want_flops = 0
+        for p in probs:
+            va, vb, _ = p.views()
+            want_flops += M.gemm(_alpha(p.label), va, vb, SCALARS["cfg2_beta"], ref[p.label[0]].view(comp=p.comp), cfg)
+        dev_c = {key: h.to_device() for key, h in shared.items()}
+        keep, calls = [], []
+        for p in probs:
+            dA, dB = p.A.to_device(), p.B.to_device()
+            keep += [dA, dB]
+            va = dA.tview(conj=p.conj_a) if p.trans_a else dA.view(conj=p.conj_a)
+            vb = dB.tview(conj=p.conj_b) if p.trans_b else dB.view(conj=p.conj_b)
+            calls.append((_alpha(p.label), va, vb, SCALARS["cfg2_beta"], dev_c[p.label[0]].view(comp=p.comp)))
+        got_flops = M.gemm_batch(calls, cfg)
+        torch.cuda.synchronize()
+        for key in shared:
+            assert dev_c[key].bytes().tobytes() == ref[key].buf.tobytes(), (c_kind, key)
+        assert got_flops == want_flops, c_kind
+        sizes = [int(x) for x in re.findall(r"batch (\d+) calls", log.read_text())]
+        assert sizes and (max(sizes) > len(calls)) == expect_split, (c_kind, sizes, len(calls))

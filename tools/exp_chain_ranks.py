@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--shard", default="chains")
     ap.add_argument("--sizes", default="256:4096:256")
+    ap.add_argument("--ranks", default="", help="only these simulated ranks (comma-separated)")
     a = ap.parse_args()
     import torch
 
@@ -45,7 +46,7 @@ def main():
     t1 = None
     for world in [int(w) for w in a.worlds.split(",")]:
         per_rank = []
-        for rank in range(world):
+        for rank in ([int(r) for r in a.ranks.split(",")] if a.ranks else range(world)):
             ops, shard, calls, call_info, a_bufs = bench.make_operands(M, items, "sweep", 0, dist_kind, dev, stream,
                                                                        world, rank, a.shard if world > 1 else "columns")
             ms = []
