@@ -167,6 +167,88 @@ __global__ void k_mix(double* dout, float* fout, int dw, int dit, int fit) {
   }
 }
 
+
+// Steady-state co-issue probe: warps [0, dw) loop on DMMA.8x8x4, the rest on
+// FFMA2 with NCH independent accumulator chains (fewer chains = a throttled
+// FP32 group), ALL until a common deadline; each group counts its iterations.
+// Unlike k_mix (fixed work per warp, one group finishing first) this gives the
+// rates while BOTH groups run: the frontier the dual-pipe kernel works against.
+template <int NCH>
+__global__ void k_steady(unsigned long long* counts, int dw, unsigned long long dur_ns) {
+  const int warp = threadIdx.x >> 5;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned long long iters = 0;
+  if (warp < dw) {
+    double a[8], b[8], c[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 1e-3 + i; b[i] = 0.5 + i; c[i][0] = c[i][1] = 0; }
+    do {
+      for (int it = 0; it < 64; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a[i]), "d"(b[i]));
+      }
+      iters += 64;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < dur_ns);
+    double r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1];
+    if (r == 1234.5) counts[2] = 1;
+    if ((threadIdx.x & 31) == 0) atomicAdd(&counts[0], iters * 8);  // DMMAs of this warp
+  } else {
+    unsigned long long acc[NCH], x[NCH];
+    float bv[NCH];
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) {
+      const float v = threadIdx.x * 1e-3f + i;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(acc[i]) : "f"(v), "f"(v + 1.0f));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(x[i]) : "f"(v * 0.5f), "f"(v * 0.25f));
+      bv[i] = 0.999f + i;
+    }
+    do {
+      for (int it = 0; it < 256; ++it) {
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          unsigned long long b;
+          asm("mov.b64 %0, {%1, %1};" : "=l"(b) : "f"(bv[i]));
+          asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[i]) : "l"(b), "l"(x[i]));
+        }
+      }
+      iters += 256;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < dur_ns);
+    float r = 0;
+#pragma unroll
+    for (int i = 0; i < NCH; ++i) r += __uint_as_float(static_cast<unsigned>(acc[i]));
+    if (r == 1234.5f) counts[2] = 1;
+    if ((threadIdx.x & 31) == 0) atomicAdd(&counts[1], iters * NCH);  // warp-wide FFMA2s of this warp
+  }
+}
+
+template <int NCH>
+static void run_steady(unsigned long long* counts, int sms, int dw, int fw, bool first) {
+  const unsigned long long dur = 2000000ull;  // 2 ms
+  unsigned long long h[3] = {0, 0, 0};
+  cudaMemset(counts, 0, 24);
+  k_steady<NCH><<<sms, 32 * (dw + fw)>>>(counts, dw, dur);  // warm-up
+  cudaDeviceSynchronize();
+  cudaMemset(counts, 0, 24);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  k_steady<NCH><<<sms, 32 * (dw + fw)>>>(counts, dw, dur);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  cudaMemcpy(h, counts, 24, cudaMemcpyDeviceToHost);
+  const double dt = double(h[0]) * (8 * 8 * 4 * 2) / (ms * 1e-3) / 1e12;
+  const double ft = double(h[1]) * 32 * 4 / (ms * 1e-3) / 1e12;
+  printf("%s\"d%d_f%d_ch%d\": [%.2f, %.2f, %.3f]", first ? "" : ", ", dw, fw, NCH, dt, ft, dt / 37.0 + ft / 72.0);
+}
+
 int main(int argc, char** argv) {
   int sms = 0, clk = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -191,6 +273,25 @@ int main(int argc, char** argv) {
       printf(", \"d%d_f%d\": [%.2f, %.2f, %.3f]", dw, fw, dt, ft, dt / 37.0 + ft / 72.0);
     }
     printf("}\n");
+    return 0;
+  }
+  if (argc > 2 && std::string(argv[2]) == "steady") {  // both groups until a common deadline
+    unsigned long long* counts;
+    CK(cudaMalloc(&counts, 24));
+    printf("{\"what\": \"[DMMA TF/s, FFMA2 TF/s, sum of fractions of 37 / 72] while both groups run (2 ms, register-only loops); dD_fF_chN = D DMMA warps + F FFMA2 warps per SM, N independent FFMA2 chains per thread\", ");
+    bool first = true;
+    for (int dw : {8, 12})
+      for (int fw : {0, 4, 8}) {
+        run_steady<8>(counts, sms, dw, fw, first); first = false;
+        if (fw) { run_steady<4>(counts, sms, dw, fw, false); run_steady<2>(counts, sms, dw, fw, false); run_steady<1>(counts, sms, dw, fw, false); }
+      }
+    run_steady<8>(counts, sms, 0, 4, false);
+    run_steady<8>(counts, sms, 0, 8, false);
+    run_steady<8>(counts, sms, 4, 4, false);
+    run_steady<8>(counts, sms, 4, 8, false);
+    run_steady<8>(counts, sms, 4, 12, false);
+    printf("}\n");
+    CK(cudaGetLastError());
     return 0;
   }
   if (argc > 2 && std::string(argv[2]) == "occ") {  // pipe rate vs resident warps per SM
