@@ -596,7 +596,7 @@ def same_config_run(M, args, stream):
     _, sample, text, dist_kind = reference_sample(args, M.Scalar)
     flops = useful_flops(sample)
     cfg = M.Config.defaults().set("gpu.numerics", args.numerics)
-    dev_ops, host_ops = [], []
+    dev_ops, host_ops, keep = [], [], []
     for i, (l, m, n, k, al, be) in enumerate(sample):
         dc, da, db = (M.dtype_from_letter(ch) for ch in l[:3])
         comp = M.SINGLE if l[3] == "s" else M.DOUBLE
@@ -608,6 +608,7 @@ def same_config_run(M, args, stream):
             (M.fill_normal if dist_kind == "normal" else M.fill_uniform)(v, state, stream)
             trip.append((t, v))
         dev_ops.append((al, trip[0][1], trip[1][1], be, trip[2][1].with_comp_prec(comp)))
+        keep.extend(t for t, _ in trip)  # the views hold raw pointers: the tensors must outlive the batch
         hs = []
         for t, v in trip:
             h = np.empty(t.numel(), np.uint8)  # pageable, like the reference's Matrix storage
@@ -640,6 +641,7 @@ def same_config_run(M, args, stream):
     el = time.perf_counter() - t0
     gc.enable()
     s1 = M.staging_bytes()
+    del keep
     return {"workload": text, "calls": len(sample), "flops_per_step": flops,
             "device_resident": {"value": device, "unit": "GFLOPS", "api": "gemm_batch on device views, CUDA events"},
             "e2e_per_call": {"value": flops * args.steps / el / 1e9, "unit": "GFLOPS",
