@@ -430,8 +430,13 @@ bool dual_schedule(std::vector<Call>& cs, const Config& cfg, DualPlan& P) {
       const bool one_sided = (td > 0) != (tf > 0);
       const bool other_left = td > 0 ? left_f > 0 : left_d > 0;
       const bool halve = one_sided && other_left;
-      const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? td / 2 : td);
-      const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? tf / 2 : tf);
+      static const double part = [] {  // tuning: MDGEMM_DUAL_ONESIDED = share of one-sided ready work taken
+        const char* f = std::getenv("MDGEMM_DUAL_ONESIDED");
+        const double v = f ? std::atof(f) : 0.5;
+        return v > 0.0 && v <= 1.0 ? v : 0.5;
+      }();
+      const double target_d = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? td * part : td);
+      const double target_f = (td > 0 && tf > 0) ? std::min(td, tf) : (halve ? tf * part : tf);
       // in priority order, whole remaining ranges that keep each side within
       // 5 % of its target; then a side that fell short takes part of its next
       // call's tiles
