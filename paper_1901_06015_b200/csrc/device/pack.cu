@@ -23,8 +23,11 @@ constexpr int PACK_THREADS = 256;
 // 44 -> 40 us, 4096 159 -> 135 us, dssd 1024 13.7 -> 12.7 us; complex sources
 // (1e / 1r, more live values) stay unbounded -- bounded they spill and run
 // slower (zzzd 4096 252 -> 258 us).  Cfg2 sweep +0.4 % (profiles/r02/pack_occupancy.txt).
+// With the loads hoisted and kept in the source type (pack_tile.cuh) six per SM
+// spills a little; five (<= 48 registers) does not: dssd 1024 14.2 -> 12.6 us,
+// dddd 4096 123.3 -> 121.9 us (profiles/r02/pack_tiles_per_cta.txt).
 #ifndef MDG_PACK_MIN_BLOCKS_REAL
-#define MDG_PACK_MIN_BLOCKS_REAL 6
+#define MDG_PACK_MIN_BLOCKS_REAL 5
 #endif
 #ifndef MDG_PACK_MIN_BLOCKS_COMPLEX
 #define MDG_PACK_MIN_BLOCKS_COMPLEX 4
@@ -35,7 +38,7 @@ constexpr int pack_min_blocks() { return SRC_COMPLEX ? MDG_PACK_MIN_BLOCKS_COMPL
 template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE>
 __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>()) pack_kernel(PackDesc d, D* __restrict__ dst) {
   __shared__ packtile::Tile tile;
-  packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS>(d, dst, blockIdx.x, tile, threadIdx.x,
+  packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS, packtile::TPC>(d, dst, blockIdx.x, tile, threadIdx.x,
                                                                    [] { __syncthreads(); });
 }
 
@@ -53,9 +56,9 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
   const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
   auto sync = [] { __syncthreads(); };
   if (d.side == MDG_SIDE_LEFT)
-    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TPC>(d, dst, bid, tile, threadIdx.x, sync);
   else
-    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TPC>(d, dst, bid, tile, threadIdx.x, sync);
 }
 
 // Packs of at least this many 32x32 tiles (a 1024^2 real operand) get their
@@ -73,10 +76,10 @@ __device__ __forceinline__ void group_tile(const PackDesc& d, void* dst, int64_t
   auto side = [&](auto fmt) {
     constexpr int FMT = decltype(fmt)::value;
     if (d.side == MDG_SIDE_LEFT)
-      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_LEFT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TPC>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
                                                                       sync);
     else
-      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TPC>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
                                                                        sync);
   };
   if constexpr (SC) {
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_group_kernel(const __gri
 
 template <typename S, bool SC, typename D, int FMT>
 cudaError_t go_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
-  const int64_t ta = packtile::pack_tiles(a), tb = packtile::pack_tiles(b);
+  const int64_t ta = packtile::pack_ctas(a), tb = packtile::pack_ctas(b);
   if (ta + tb == 0) return cudaSuccess;
   if (ta + tb > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   pack_pair_kernel<S, SC, D, FMT><<<static_cast<unsigned>(ta + tb), PACK_THREADS, 0, s>>>(
@@ -151,7 +154,7 @@ cudaError_t pad(const PackDesc& d, void* dst, cudaStream_t s) {
 
 template <typename S, bool SC, typename D, int FMT>
 cudaError_t go_side(const PackDesc& d, void* dst, cudaStream_t s) {
-  const int64_t tiles = packtile::pack_tiles(d);
+  const int64_t tiles = packtile::pack_ctas(d);
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned>(tiles));
@@ -212,8 +215,8 @@ cudaError_t launch_pack_group(PackGroup& g, cudaStream_t s) {
   g.n = keep;
   int64_t tiles = 0;
   for (int j = 0; j < g.n; ++j) {
-    g.tile0[j] = tiles;
-    tiles += packtile::pack_tiles(g.d[j]);
+    g.tile0[j] = tiles;  // in CTAs (TPC source tiles each)
+    tiles += packtile::pack_ctas(g.d[j]);
   }
   g.tile0[g.n] = tiles;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;

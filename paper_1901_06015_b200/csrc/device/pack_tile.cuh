@@ -8,6 +8,8 @@
 // axis.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace mdg {
@@ -16,13 +18,33 @@ namespace packtile {
 constexpr int TILE = 32;
 using Tile = double2[TILE][TILE + 1];
 
+// A source element as loaded (its own type: a thread keeps several loads in
+// flight, and a float costs one register where the widened pair costs four).
 template <typename S, bool SRC_COMPLEX>
-__device__ __forceinline__ double2 load_src(const DView& v, int64_t i, int64_t j) {
+struct Raw {
+  S re, im;
+};
+template <typename S>
+struct Raw<S, false> {
+  S re;
+};
+
+template <typename S, bool SRC_COMPLEX>
+__device__ __forceinline__ Raw<S, SRC_COMPLEX> load_raw(const DView& v, int64_t i, int64_t j) {
   const S* p = reinterpret_cast<const S*>(v.base) + (i * v.rs + j * v.cs) * (SRC_COMPLEX ? 2 : 1);
   if constexpr (SRC_COMPLEX) {
-    return make_double2(static_cast<double>(p[0]), static_cast<double>(p[1]));
+    return Raw<S, true>{p[0], p[1]};  // two loads: a complex element is only aligned to its real type
   } else {
-    return make_double2(static_cast<double>(p[0]), 0.0);
+    return Raw<S, false>{p[0]};
+  }
+}
+
+template <typename S, bool SRC_COMPLEX>
+__device__ __forceinline__ double2 widen(const Raw<S, SRC_COMPLEX>& r) {
+  if constexpr (SRC_COMPLEX) {
+    return make_double2(static_cast<double>(r.re), static_cast<double>(r.im));
+  } else {
+    return make_double2(static_cast<double>(r.re), 0.0);
   }
 }
 
@@ -95,66 +117,85 @@ __device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ ds
   }
 }
 
-// Tile `bid` (source tiles column-major over ext_i x ext_j) by NT threads
-// (thread t of NT); sync() separates the staging from the stores.  When the
+// Source tiles TPC * bid .. TPC * bid + TPC - 1 (source tiles column-major over
+// ext_i x ext_j) by NT threads (thread t of NT); sync() separates the staging
+// from the stores.  The thread issues all its loads, kept in the source's own
+// type, before it converts or stages anything (the transposing path used to
+// convert and stage each element as it arrived: zzzd 4096 packs 252 -> 221 us,
+// dddd 4096 135 -> 124 us).  When the
 // source's unit-stride axis is the packed panels' contiguous axis (a left
 // pack of a column-major A, a right pack of a row-major B) the tile needs no
 // transpose: each element goes straight from its load to its store, both
 // coalesced, with no shared-memory round trip or barrier.
-template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE, int NT, class Sync>
+template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE, int NT, int TPC, class Sync>
 __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst, int64_t bid, Tile& tile, int t,
                                           Sync sync) {
   constexpr int ROWS = NT / 32;  // warps: tile rows per pass
+  constexpr int PER = TILE / ROWS;
   const int64_t tiles_i = (d.ext_i + TILE - 1) / TILE;
-  const int64_t i0 = (bid % tiles_i) * TILE;
-  const int64_t j0 = (bid / tiles_i) * TILE;
+  const int64_t tiles = tiles_i * ((d.ext_j + TILE - 1) / TILE);
   const int lane = t & 31, row = t >> 5;
   const bool i_fast = d.src.rs <= d.src.cs;
+  int64_t i0[TPC], j0[TPC];
+#pragma unroll
+  for (int u = 0; u < TPC; ++u) {
+    const int64_t tb = bid * TPC + u;  // past the last tile: no element passes the extent tests below
+    i0[u] = tb < tiles ? (tb % tiles_i) * TILE : d.ext_i;
+    j0[u] = tb < tiles ? (tb / tiles_i) * TILE : d.ext_j;
+  }
+  // all of the thread's loads in flight before the first store (or staging)
+  Raw<S, SRC_COMPLEX> raw[TPC][PER];
+#pragma unroll
+  for (int u = 0; u < TPC; ++u)
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int ii = i_fast ? lane : row + ROWS * r;
+      const int jj = i_fast ? row + ROWS * r : lane;
+      const int64_t i = i0[u] + ii, j = j0[u] + jj;
+      raw[u][r] = Raw<S, SRC_COMPLEX>{};
+      if (i < d.src.m && j < d.src.n) raw[u][r] = load_raw<S, SRC_COMPLEX>(d.src, i, j);
+    }
 
   if (i_fast == (SIDE == MDG_SIDE_LEFT)) {  // no transpose (uniform per launch)
-    // all of the thread's loads in flight before the first store
-    double2 raw[TILE / ROWS];
 #pragma unroll
-    for (int r = 0; r < TILE / ROWS; ++r) {
-      const int ii = i_fast ? lane : row + ROWS * r;
-      const int jj = i_fast ? row + ROWS * r : lane;
-      const int64_t i = i0 + ii, j = j0 + jj;
-      raw[r] = make_double2(0.0, 0.0);
-      if (i < d.src.m && j < d.src.n) raw[r] = load_src<S, SRC_COMPLEX>(d.src, i, j);
-    }
+    for (int u = 0; u < TPC; ++u)
 #pragma unroll
-    for (int r = 0; r < TILE / ROWS; ++r) {
-      const int ii = i_fast ? lane : row + ROWS * r;
-      const int jj = i_fast ? row + ROWS * r : lane;
-      const int64_t i = i0 + ii, j = j0 + jj;
-      if (i >= d.ext_i || j >= d.ext_j) continue;
-      // padded slots take literal zeros (not processed: the reference pads with +0 / -0 as stored)
-      const double2 v = (i < d.src.m && j < d.src.n) ? process(raw[r], d) : make_double2(0.0, 0.0);
-      put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, v);
-    }
+      for (int r = 0; r < PER; ++r) {
+        const int ii = i_fast ? lane : row + ROWS * r;
+        const int jj = i_fast ? row + ROWS * r : lane;
+        const int64_t i = i0[u] + ii, j = j0[u] + jj;
+        if (i >= d.ext_i || j >= d.ext_j) continue;
+        // padded slots take literal zeros (not processed: the reference pads with +0 / -0 as stored)
+        const double2 v =
+            (i < d.src.m && j < d.src.n) ? process(widen<S, SRC_COMPLEX>(raw[u][r]), d) : make_double2(0.0, 0.0);
+        put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, v);
+      }
     return;
   }
 
-  // Load: coalesce along the source's unit-stride axis.
 #pragma unroll
-  for (int r = 0; r < TILE / ROWS; ++r) {
-    const int ii = i_fast ? lane : row + ROWS * r;
-    const int jj = i_fast ? row + ROWS * r : lane;
-    const int64_t i = i0 + ii, j = j0 + jj;
-    double2 v = make_double2(0.0, 0.0);  // padded slots take literal zeros
-    if (i < d.src.m && j < d.src.n) v = process(load_src<S, SRC_COMPLEX>(d.src, i, j), d);
-    tile[jj][ii] = v;
-  }
-  sync();
-
-  // Store: coalesce along the packed buffer's contiguous axis.
+  for (int u = 0; u < TPC; ++u) {
+    if (bid * TPC + u >= tiles) break;  // uniform per CTA
+    if (u > 0) sync();                  // the previous tile's stores have read the staging tile
+    // Stage: the loads were coalesced along the source's unit-stride axis.
 #pragma unroll
-  for (int r = 0; r < TILE / ROWS; ++r) {
-    const int ii = SIDE == MDG_SIDE_LEFT ? lane : row + ROWS * r;
-    const int jj = SIDE == MDG_SIDE_LEFT ? row + ROWS * r : lane;
-    const int64_t i = i0 + ii, j = j0 + jj;
-    if (i >= d.ext_i || j >= d.ext_j) continue;
-    put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, tile[jj][ii]);
+    for (int r = 0; r < PER; ++r) {
+      const int ii = i_fast ? lane : row + ROWS * r;
+      const int jj = i_fast ? row + ROWS * r : lane;
+      const int64_t i = i0[u] + ii, j = j0[u] + jj;
+      // padded slots take literal zeros
+      tile[jj][ii] = (i < d.src.m && j < d.src.n) ? process(widen<S, SRC_COMPLEX>(raw[u][r]), d) : make_double2(0.0, 0.0);
+    }
+    sync();
+    // Store: coalesce along the packed buffer's contiguous axis.
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int ii = SIDE == MDG_SIDE_LEFT ? lane : row + ROWS * r;
+      const int jj = SIDE == MDG_SIDE_LEFT ? row + ROWS * r : lane;
+      const int64_t i = i0[u] + ii, j = j0[u] + jj;
+      if (i >= d.ext_i || j >= d.ext_j) continue;
+      put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, tile[jj][ii]);
+    }
   }
 }
 
@@ -162,6 +203,17 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
 __host__ __device__ inline int64_t pack_tiles(const PackDesc& d) {
   return ((d.ext_i + TILE - 1) / TILE) * ((d.ext_j + TILE - 1) / TILE);
 }
+
+// Source tiles per CTA, and the CTAs of a pack.  Measured on B200
+// (profiles/r02/pack_tiles_per_cta.txt): one tile per CTA with its loads
+// hoisted beats two or four -- a fat CTA's staging / store phases no longer
+// overlap other CTAs' loads, and its index state spills at the six-CTA
+// register bound (dddd 4096 pack pair 124 / 148 / 154 us at 1 / 2 / 4).
+#ifndef MDG_PACK_TPC
+#define MDG_PACK_TPC 1
+#endif
+constexpr int TPC = MDG_PACK_TPC;
+__host__ __device__ inline int64_t pack_ctas(const PackDesc& d) { return (pack_tiles(d) + TPC - 1) / TPC; }
 
 }  // namespace packtile
 }  // namespace mdg
