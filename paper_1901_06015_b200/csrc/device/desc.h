@@ -80,6 +80,8 @@ struct PackDesc {
   int32_t pd_shift;        // log2(pd) when pd is a power of two, else -1
   int32_t pitch;           // elements between consecutive panel lines (= pd: the reference layout;
                            // wider: padded lines, the dual kernel's conflict-free D stages)
+  int32_t vec;             // set by the pack launchers: 16-byte vector tiles (pack_tile.cuh: vec_ok)
+  int32_t pad_;
 };
 
 // Exact (reference-replaying) gemm modes.

@@ -8,6 +8,7 @@
 // coalesced along the source's unit-stride axis and written coalesced along
 // the packed buffer's contiguous axis (rows for left panels, columns for
 // right panels), so a transposing pack costs one HBM read and one HBM write.
+#include <cstdlib>
 #include <type_traits>
 
 #include "pack_tile.cuh"
@@ -27,7 +28,7 @@ constexpr int PACK_THREADS = 256;
 // spills a little; five (<= 48 registers) does not: dssd 1024 14.2 -> 12.6 us,
 // dddd 4096 123.3 -> 121.9 us (profiles/r02/pack_tiles_per_cta.txt).
 #ifndef MDG_PACK_MIN_BLOCKS_REAL
-#define MDG_PACK_MIN_BLOCKS_REAL 5
+#define MDG_PACK_MIN_BLOCKS_REAL 4
 #endif
 #ifndef MDG_PACK_MIN_BLOCKS_COMPLEX
 #define MDG_PACK_MIN_BLOCKS_COMPLEX 4
@@ -38,6 +39,12 @@ constexpr int pack_min_blocks() { return SRC_COMPLEX ? MDG_PACK_MIN_BLOCKS_COMPL
 template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE>
 __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>()) pack_kernel(PackDesc d, D* __restrict__ dst) {
   __shared__ packtile::Tile tile;
+  if constexpr (!SRC_COMPLEX && FMT == MDG_FMT_STANDARD) {
+    if (d.vec) {  // uniform per launch
+      packtile::pack_tile_vec<S, D, SIDE, PACK_THREADS>(d, dst, blockIdx.x, tile, threadIdx.x, [] { __syncthreads(); });
+      return;
+    }
+  }
   packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS, packtile::TPC>(d, dst, blockIdx.x, tile, threadIdx.x,
                                                                    [] { __syncthreads(); });
 }
@@ -55,6 +62,13 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
   D* dst = first ? dst0 : dst1;
   const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
   auto sync = [] { __syncthreads(); };
+  if constexpr (!SRC_COMPLEX && FMT == MDG_FMT_STANDARD) {
+    if (d.vec) {  // uniform per CTA
+      if (d.side == MDG_SIDE_LEFT) packtile::pack_tile_vec<S, D, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+      else packtile::pack_tile_vec<S, D, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+      return;
+    }
+  }
   if (d.side == MDG_SIDE_LEFT)
     packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TPC>(d, dst, bid, tile, threadIdx.x, sync);
   else
@@ -73,6 +87,15 @@ constexpr int64_t kGroupLargeTiles = 1024;
 template <typename S, bool SC, typename D>
 __device__ __forceinline__ void group_tile(const PackDesc& d, void* dst, int64_t bid, packtile::Tile& tile) {
   auto sync = [] { __syncthreads(); };
+  if constexpr (!SC) {
+    if (d.vec) {  // uniform per CTA
+      if (d.side == MDG_SIDE_LEFT)
+        packtile::pack_tile_vec<S, D, MDG_SIDE_LEFT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x, sync);
+      else
+        packtile::pack_tile_vec<S, D, MDG_SIDE_RIGHT, PACK_THREADS>(d, static_cast<D*>(dst), bid, tile, threadIdx.x, sync);
+      return;
+    }
+  }
   auto side = [&](auto fmt) {
     constexpr int FMT = decltype(fmt)::value;
     if (d.side == MDG_SIDE_LEFT)
@@ -116,8 +139,23 @@ __global__ void __launch_bounds__(PACK_THREADS, 4) pack_group_kernel(const __gri
   }
 }
 
+// Vector tiles where the pack allows them (MDGEMM_PACK_VEC=0: scalar tiles only, A/B runs).
+bool vec_enabled() {
+  static const bool on = [] {
+    const char* f = std::getenv("MDGEMM_PACK_VEC");
+    return !(f && std::atoi(f) == 0);
+  }();
+  return on;
+}
+PackDesc with_vec(const PackDesc& d, const void* dst) {
+  PackDesc o = d;
+  o.vec = vec_enabled() && packtile::vec_ok(d, dst) ? 1 : 0;
+  return o;
+}
+
 template <typename S, bool SC, typename D, int FMT>
-cudaError_t go_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
+cudaError_t go_pair(const PackDesc& a0, void* da, const PackDesc& b0, void* db, cudaStream_t s) {
+  const PackDesc a = with_vec(a0, da), b = with_vec(b0, db);
   const int64_t ta = packtile::pack_ctas(a), tb = packtile::pack_ctas(b);
   if (ta + tb == 0) return cudaSuccess;
   if (ta + tb > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -153,7 +191,8 @@ cudaError_t pad(const PackDesc& d, void* dst, cudaStream_t s) {
 }
 
 template <typename S, bool SC, typename D, int FMT>
-cudaError_t go_side(const PackDesc& d, void* dst, cudaStream_t s) {
+cudaError_t go_side(const PackDesc& d0, void* dst, cudaStream_t s) {
+  const PackDesc d = with_vec(d0, dst);
   const int64_t tiles = packtile::pack_ctas(d);
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
@@ -215,7 +254,8 @@ cudaError_t launch_pack_group(PackGroup& g, cudaStream_t s) {
   g.n = keep;
   int64_t tiles = 0;
   for (int j = 0; j < g.n; ++j) {
-    g.tile0[j] = tiles;  // in CTAs (TPC source tiles each)
+    g.d[j] = with_vec(g.d[j], g.dst[j]);
+    g.tile0[j] = tiles;  // in CTAs (TPC source tiles each, or one vector tile)
     tiles += packtile::pack_ctas(g.d[j]);
   }
   g.tile0[g.n] = tiles;
