@@ -81,7 +81,8 @@ struct PackDesc {
   int32_t pitch;           // elements between consecutive panel lines (= pd: the reference layout;
                            // wider: padded lines, the dual kernel's conflict-free D stages)
   int32_t vec;             // set by the pack launchers: 16-byte vector tiles (pack_tile.cuh: vec_ok)
-  int32_t pad_;
+  int32_t cvec;            // set by the pack launchers: complex source elements aligned to their own size
+                           // (one 8- / 16-byte load per element instead of two)
 };
 
 // Exact (reference-replaying) gemm modes.

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>()) 
       return;
     }
   }
-  packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS, packtile::TPC>(d, dst, blockIdx.x, tile, threadIdx.x,
+  packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS, packtile::TpcOf<S, SRC_COMPLEX>::value>(d, dst, blockIdx.x, tile, threadIdx.x,
                                                                    [] { __syncthreads(); });
 }
 
@@ -70,9 +70,9 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
     }
   }
   if (d.side == MDG_SIDE_LEFT)
-    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TPC>(d, dst, bid, tile, threadIdx.x, sync);
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TpcOf<S, SRC_COMPLEX>::value>(d, dst, bid, tile, threadIdx.x, sync);
   else
-    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TPC>(d, dst, bid, tile, threadIdx.x, sync);
+    packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TpcOf<S, SRC_COMPLEX>::value>(d, dst, bid, tile, threadIdx.x, sync);
 }
 
 // Packs of at least this many 32x32 tiles (a 1024^2 real operand) get their
@@ -99,10 +99,10 @@ __device__ __forceinline__ void group_tile(const PackDesc& d, void* dst, int64_t
   auto side = [&](auto fmt) {
     constexpr int FMT = decltype(fmt)::value;
     if (d.side == MDG_SIDE_LEFT)
-      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TPC>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TpcOf<S, SC>::value>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
                                                                       sync);
     else
-      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TPC>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
+      packtile::pack_tile<S, SC, D, FMT, MDG_SIDE_RIGHT, PACK_THREADS, packtile::TpcOf<S, SC>::value>(d, static_cast<D*>(dst), bid, tile, threadIdx.x,
                                                                        sync);
   };
   if constexpr (SC) {
@@ -150,6 +150,8 @@ bool vec_enabled() {
 PackDesc with_vec(const PackDesc& d, const void* dst) {
   PackDesc o = d;
   o.vec = vec_enabled() && packtile::vec_ok(d, dst) ? 1 : 0;
+  const uint64_t csz = d.src.dtype == MDG_DT_C ? 8 : d.src.dtype == MDG_DT_Z ? 16 : 0;
+  o.cvec = vec_enabled() && csz != 0 && reinterpret_cast<uint64_t>(d.src.base) % csz == 0 ? 1 : 0;
   return o;
 }
 

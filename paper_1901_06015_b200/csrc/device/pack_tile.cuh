@@ -30,10 +30,15 @@ struct Raw<S, false> {
 };
 
 template <typename S, bool SRC_COMPLEX>
-__device__ __forceinline__ Raw<S, SRC_COMPLEX> load_raw(const DView& v, int64_t i, int64_t j) {
+__device__ __forceinline__ Raw<S, SRC_COMPLEX> load_raw(const DView& v, int64_t i, int64_t j, bool cvec) {
   const S* p = reinterpret_cast<const S*>(v.base) + (i * v.rs + j * v.cs) * (SRC_COMPLEX ? 2 : 1);
   if constexpr (SRC_COMPLEX) {
-    return Raw<S, true>{p[0], p[1]};  // two loads: a complex element is only aligned to its real type
+    if (cvec) {  // the base is aligned to the complex element (uniform per launch): one load
+      using V = typename std::conditional<sizeof(S) == 4, float2, double2>::type;
+      const V q = *reinterpret_cast<const V*>(p);
+      return Raw<S, true>{q.x, q.y};
+    }
+    return Raw<S, true>{p[0], p[1]};  // a complex element is only guaranteed the alignment of its real type
   } else {
     return Raw<S, false>{p[0]};
   }
@@ -153,7 +158,7 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
       const int jj = i_fast ? row + ROWS * r : lane;
       const int64_t i = i0[u] + ii, j = j0[u] + jj;
       raw[u][r] = Raw<S, SRC_COMPLEX>{};
-      if (i < d.src.m && j < d.src.n) raw[u][r] = load_raw<S, SRC_COMPLEX>(d.src, i, j);
+      if (i < d.src.m && j < d.src.n) raw[u][r] = load_raw<S, SRC_COMPLEX>(d.src, i, j, d.cvec != 0);
     }
 
   if (i_fast == (SIDE == MDG_SIDE_LEFT)) {  // no transpose (uniform per launch)
@@ -360,14 +365,22 @@ __host__ __device__ inline int64_t pack_tiles(const PackDesc& d) {
 #ifndef MDG_PACK_TPC
 #define MDG_PACK_TPC 1
 #endif
-constexpr int TPC = MDG_PACK_TPC;
+#ifndef MDG_PACK_TPC_C
+#define MDG_PACK_TPC_C 1
+#endif
+// per source type: complex single sources (8-byte elements) may take their own count
+template <typename S, bool SRC_COMPLEX>
+struct TpcOf {
+  static constexpr int value = SRC_COMPLEX && sizeof(S) == 4 ? MDG_PACK_TPC_C : MDG_PACK_TPC;
+};
 __host__ __device__ inline int64_t pack_ctas(const PackDesc& d) {
   if (d.vec) {
     const bool ss = d.src.dtype == MDG_DT_S, ts = d.target_single != 0;
     return ss ? (ts ? vec_tiles<float, float>(d) : vec_tiles<float, double>(d))
               : (ts ? vec_tiles<double, float>(d) : vec_tiles<double, double>(d));
   }
-  return (pack_tiles(d) + TPC - 1) / TPC;
+  const int tpc = d.src.dtype == MDG_DT_C ? MDG_PACK_TPC_C : MDG_PACK_TPC;
+  return (pack_tiles(d) + tpc - 1) / tpc;
 }
 
 }  // namespace packtile
