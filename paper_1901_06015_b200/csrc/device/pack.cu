@@ -57,8 +57,17 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
     pack_pair_kernel(const __grid_constant__ PackDesc d0, D* __restrict__ dst0, const __grid_constant__ PackDesc d1,
                      D* __restrict__ dst1, int64_t tiles0) {
   __shared__ packtile::Tile tile;
+  __shared__ PackDesc sd;  // this CTA's pack (selecting between the two parameter structs by reference
+                           // makes ptxas copy both to local memory)
   const bool first = static_cast<int64_t>(blockIdx.x) < tiles0;
-  const PackDesc& d = first ? d0 : d1;
+  static_assert(sizeof(PackDesc) % 4 == 0, "PackDesc copied as words");
+  if (threadIdx.x < sizeof(PackDesc) / 4) {
+    const uint32_t w0 = reinterpret_cast<const uint32_t*>(&d0)[threadIdx.x];
+    const uint32_t w1 = reinterpret_cast<const uint32_t*>(&d1)[threadIdx.x];
+    reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = first ? w0 : w1;
+  }
+  __syncthreads();
+  const PackDesc& d = sd;
   D* dst = first ? dst0 : dst1;
   const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
   auto sync = [] { __syncthreads(); };
