@@ -94,3 +94,35 @@ def test_pack_errors_surface_as_error():
     zsrc = HostMatrix(M.DT_Z, 2, 2).fill(1).to_device()
     with pytest.raises(M.Error):
         M.pack_block_device(buf.data_ptr(), zsrc.view(), M.LEFT, M.STANDARD, 0, SCALARS["c55"], M.DT_Z, 4)
+
+
+@pytest.mark.parametrize("dt", [M.DT_S, M.DT_D])
+@pytest.mark.parametrize("side", [M.LEFT, M.RIGHT])
+@pytest.mark.parametrize("tp", [M.SINGLE, M.DOUBLE])
+def test_pack_vector_tiles(dt, side, tp):
+    """Real sources with a unit-stride axis and 16-byte aligned lines take the vector tiles
+    (pack_tile.cuh: vec_ok / pack_tile_vec): sub-blocks of a parent matrix whose leading
+    dimension is a multiple of four elements, extents that end inside a vector, inside a tile and
+    past several tiles, aligned and unaligned origins (the latter fall back to scalar tiles),
+    both storage orders (= both the straight and the transposing path per side)."""
+    import torch
+    es = M.dtype_size(dt)
+    for (pm, pn), (m, n), (oi, oj), kind, rb, plen, sc in itertools.product(
+            [(48, 80), (260, 300)], [(33, 70), (47, 5), (1, 64), (250, 290)], [(0, 0), (4, 2), (1, 0)],
+            ["col", "row"], [4, 64, 128], [0, 1], ["one", "p7"]):
+        if oi + m > pm or oj + n > pn:
+            continue
+        parent = HostMatrix(dt, pm, pn, kind).fill(O.orc_rng_state(13, ["vec", dt, kind, pm]))
+        off = (oi * parent.rs + oj * parent.cs) * es
+        hv = M.MatrixView.make(parent.buf.ctypes.data + off, m, n, parent.rs, parent.cs, dt)
+        dev = torch.from_numpy(parent.buf.copy()).cuda()
+        dv = M.MatrixView.make(dev.data_ptr() + off, m, n, parent.rs, parent.cs, dt)
+        pl = 2 * max(m, n) + 16 if plen else 0
+        nbytes = O.orc_packed_bytes(hv, side, M.STANDARD, tp, rb, pl)
+        assert nbytes == M.packed_bytes(dv, side, M.STANDARD, tp, rb, pl)
+        want = np.full(nbytes, 0xA5, np.uint8)
+        O.orc_pack(hv, side, M.STANDARD, 0, SCALARS[sc], tp, rb, pl, want.ctypes.data)
+        out = torch.full((nbytes,), 0x5A, dtype=torch.uint8, device="cuda")
+        M.pack_block_device(out.data_ptr(), dv, side, M.STANDARD, 0, SCALARS[sc], tp, rb, pl)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == want.tobytes(), (pm, pn, m, n, oi, oj, kind, rb, plen, sc)
