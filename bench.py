@@ -445,6 +445,9 @@ def run_b200(args):
         serial_peak = (fd + ff) / (fd / pk["dmma_tflops"] + ff / pk["ffma_tflops"]) if fd + ff else 0.0
         roof = {"bound": "tensor", "achieved": achieved, "peak": serial_peak, "unit": "TFLOP/s",
                 "frac": achieved / serial_peak if serial_peak else 0.0, "traffic": traffic_map.get("dual"),
+                "traffic_scope": "DRAM bytes of ONE captured launch of the 3584/4096 sweep slice (ncu --set full, "
+                                 "12.6 ms: 0.48 TB/s, 6 % of the HBM rate -- the kernel is pipe-bound); achieved / peak are "
+                                 "flops over all launches of the step",
                 "kernel": "gemm_dual: FP64 DMMA.8x8x4 warps + FP32 FFMA2 warps on every SM at once",
                 "pipes": {"dmma": {"achieved": fd / (ms * 1e-3) / 1e12, "peak": pk["dmma_tflops"],
                                    "frac": fd / (ms * 1e-3) / 1e12 / pk["dmma_tflops"]},
