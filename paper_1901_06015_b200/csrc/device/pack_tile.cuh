@@ -80,10 +80,33 @@ struct Pair<double> {
   static __device__ __forceinline__ T make(double a, double b) { return make_double2(a, b); }
 };
 
+// The element pipeline on a loaded element, result in the target type.  With
+// a unit scale the pipeline is widen -> conj -> round to the target: one
+// conversion of the source value (none when the types agree) gives the same
+// bits, and a float -> float pack no longer spends four F2F conversions per
+// element on a round trip through double.
+template <typename S, bool SRC_COMPLEX, typename D>
+__device__ __forceinline__ typename Pair<D>::T process_typed(const Raw<S, SRC_COMPLEX>& r, const PackDesc& d) {
+  if (d.unit_scale) {  // uniform per launch
+    typename Pair<D>::T o;
+    o.x = static_cast<D>(r.re);
+    if constexpr (SRC_COMPLEX) {
+      const D im = static_cast<D>(r.im);
+      o.y = d.do_conj ? -im : im;
+    } else {
+      o.y = d.do_conj ? -D(0) : D(0);
+    }
+    return o;
+  }
+  const double2 v = process(widen<S, SRC_COMPLEX>(r), d);
+  return Pair<D>::make(v.x, v.y);
+}
+
 // Store one processed source element (i, j) -- packed-logical row / column
 // of the block -- in the panel layout of FMT / SIDE.
 template <typename D, bool SRC_COMPLEX, int FMT, int SIDE>
-__device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ dst, int64_t i, int64_t j, double2 v) {
+__device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ dst, int64_t i, int64_t j,
+                                           typename Pair<D>::T v) {
   const int64_t PD = d.pd, LP = d.lpad, PT = d.pitch;
   // offset of packed-logical (pr, pc) in block elements; power-of-two panel
   // dims (every kernel tile) avoid the 64-bit division per element
@@ -96,28 +119,28 @@ __device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ ds
   };
   if constexpr (FMT == MDG_FMT_STANDARD) {
     if constexpr (SRC_COMPLEX) {
-      reinterpret_cast<typename Pair<D>::T*>(dst)[off(i, j)] = Pair<D>::make(v.x, v.y);
+      reinterpret_cast<typename Pair<D>::T*>(dst)[off(i, j)] = v;
     } else {
-      dst[off(i, j)] = static_cast<D>(v.x);
+      dst[off(i, j)] = v.x;
     }
   } else if constexpr (FMT == MDG_FMT_ONEE) {
     using P = typename Pair<D>::T;
     if constexpr (SIDE == MDG_SIDE_LEFT) {
       // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, -im], [im, re]]
-      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
-      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j + 1)) = Pair<D>::make(-v.y, v.x);
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = v;
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j + 1)) = P{-v.y, v.x};
     } else {
       // rows (2i, 2i+1) x cols (2j, 2j+1) = [[re, im], [-im, re]]
-      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = Pair<D>::make(v.x, v.y);
-      *reinterpret_cast<P*>(dst + off(2 * i + 1, 2 * j)) = Pair<D>::make(-v.y, v.x);
+      *reinterpret_cast<P*>(dst + off(2 * i, 2 * j)) = v;
+      *reinterpret_cast<P*>(dst + off(2 * i + 1, 2 * j)) = P{-v.y, v.x};
     }
   } else {  // 1r
     if constexpr (SIDE == MDG_SIDE_LEFT) {
-      dst[off(i, 2 * j)] = static_cast<D>(v.x);
-      dst[off(i, 2 * j + 1)] = static_cast<D>(v.y);
+      dst[off(i, 2 * j)] = v.x;
+      dst[off(i, 2 * j + 1)] = v.y;
     } else {
-      dst[off(2 * i, j)] = static_cast<D>(v.x);
-      dst[off(2 * i + 1, j)] = static_cast<D>(v.y);
+      dst[off(2 * i, j)] = v.x;
+      dst[off(2 * i + 1, j)] = v.y;
     }
   }
 }
@@ -171,13 +194,15 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
         const int64_t i = i0[u] + ii, j = j0[u] + jj;
         if (i >= d.ext_i || j >= d.ext_j) continue;
         // padded slots take literal zeros (not processed: the reference pads with +0 / -0 as stored)
-        const double2 v =
-            (i < d.src.m && j < d.src.n) ? process(widen<S, SRC_COMPLEX>(raw[u][r]), d) : make_double2(0.0, 0.0);
+        const typename Pair<D>::T v =
+            (i < d.src.m && j < d.src.n) ? process_typed<S, SRC_COMPLEX, D>(raw[u][r], d) : typename Pair<D>::T{D(0), D(0)};
         put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, v);
       }
     return;
   }
 
+  // the staging tile in the target type
+  typename Pair<D>::T(*st)[TILE + 1] = reinterpret_cast<typename Pair<D>::T(*)[TILE + 1]>(&tile[0][0]);
 #pragma unroll
   for (int u = 0; u < TPC; ++u) {
     if (bid * TPC + u >= tiles) break;  // uniform per CTA
@@ -189,7 +214,7 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
       const int jj = i_fast ? row + ROWS * r : lane;
       const int64_t i = i0[u] + ii, j = j0[u] + jj;
       // padded slots take literal zeros
-      tile[jj][ii] = (i < d.src.m && j < d.src.n) ? process(widen<S, SRC_COMPLEX>(raw[u][r]), d) : make_double2(0.0, 0.0);
+      st[jj][ii] = (i < d.src.m && j < d.src.n) ? process_typed<S, SRC_COMPLEX, D>(raw[u][r], d) : typename Pair<D>::T{D(0), D(0)};
     }
     sync();
     // Store: coalesce along the packed buffer's contiguous axis.
@@ -199,7 +224,7 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
       const int jj = SIDE == MDG_SIDE_LEFT ? row + ROWS * r : lane;
       const int64_t i = i0[u] + ii, j = j0[u] + jj;
       if (i >= d.ext_i || j >= d.ext_j) continue;
-      put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, tile[jj][ii]);
+      put_packed<D, SRC_COMPLEX, FMT, SIDE>(d, dst, i, j, st[jj][ii]);
     }
   }
 }
@@ -301,7 +326,7 @@ __device__ __forceinline__ void pack_tile_vec(const PackDesc& d, D* __restrict__
   // element (c + v, l) of the source index space: processed inside the source, a literal zero in the padding
   auto value = [&](int r, int v) -> D {
     const int64_t l = l0 + row + ROWS * r;
-    if (l < src_l && c + v < src_c) return static_cast<D>(process(make_double2(static_cast<double>(raw[r].e[v]), 0.0), d).x);
+    if (l < src_l && c + v < src_c) return process_typed<S, false, D>(Raw<S, false>{raw[r].e[v]}, d).x;
     return D(0);
   };
 
