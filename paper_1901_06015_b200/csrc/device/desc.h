@@ -83,6 +83,8 @@ struct PackDesc {
   int32_t vec;             // set by the pack launchers: 16-byte vector tiles (pack_tile.cuh: vec_ok)
   int32_t cvec;            // set by the pack launchers: complex source elements aligned to their own size
                            // (one 8- / 16-byte load per element instead of two)
+  int32_t interior;        // set by the pack launchers: tiles inside the source take the 32-bit index path
+  int32_t pad_;
 };
 
 // Exact (reference-replaying) gemm modes.

@@ -161,6 +161,9 @@ PackDesc with_vec(const PackDesc& d, const void* dst) {
   o.vec = vec_enabled() && packtile::vec_ok(d, dst) ? 1 : 0;
   const uint64_t csz = d.src.dtype == MDG_DT_C ? 8 : d.src.dtype == MDG_DT_Z ? 16 : 0;
   o.cvec = vec_enabled() && csz != 0 && reinterpret_cast<uint64_t>(d.src.base) % csz == 0 ? 1 : 0;
+  // 32-bit offsets inside a tile: the line pitches must leave 63 lines of a tile inside 2^31 elements
+  o.interior = vec_enabled() && d.src.rs >= 0 && d.src.cs >= 0 && d.src.rs < (int64_t{1} << 24) &&
+               d.src.cs < (int64_t{1} << 24) && d.pitch < (1 << 24) ? 1 : 0;
   return o;
 }
 
