@@ -39,14 +39,41 @@ constexpr int pack_min_blocks() { return SRC_COMPLEX ? MDG_PACK_MIN_BLOCKS_COMPL
 template <typename S, bool SRC_COMPLEX, typename D, int FMT, int SIDE>
 __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>()) pack_kernel(PackDesc d, D* __restrict__ dst) {
   __shared__ packtile::Tile tile;
-  if constexpr (!SRC_COMPLEX && FMT == MDG_FMT_STANDARD) {
-    if (d.vec) {  // uniform per launch
-      packtile::pack_tile_vec<S, D, SIDE, PACK_THREADS>(d, dst, blockIdx.x, tile, threadIdx.x, [] { __syncthreads(); });
-      return;
-    }
-  }
   packtile::pack_tile<S, SRC_COMPLEX, D, FMT, SIDE, PACK_THREADS, packtile::TpcOf<S, SRC_COMPLEX>::value>(d, dst, blockIdx.x, tile, threadIdx.x,
                                                                    [] { __syncthreads(); });
+}
+
+// The vector tiles of a real source (PackDesc.vec), in kernels of their own: next to the scalar paths
+// they cost both register budgets.
+#ifndef MDG_PACK_VEC_BLOCKS
+#define MDG_PACK_VEC_BLOCKS 4
+#endif
+template <typename S, typename D, int SIDE>
+__global__ void __launch_bounds__(PACK_THREADS, MDG_PACK_VEC_BLOCKS) pack_vec_kernel(PackDesc d, D* __restrict__ dst) {
+  __shared__ packtile::Tile tile;
+  packtile::pack_tile_vec<S, D, SIDE, PACK_THREADS>(d, dst, blockIdx.x, tile, threadIdx.x, [] { __syncthreads(); });
+}
+
+template <typename S, typename D>
+__global__ void __launch_bounds__(PACK_THREADS, MDG_PACK_VEC_BLOCKS)
+    pack_pair_vec_kernel(const __grid_constant__ PackDesc d0, D* __restrict__ dst0, const __grid_constant__ PackDesc d1,
+                         D* __restrict__ dst1, int64_t tiles0) {
+  __shared__ packtile::Tile tile;
+  __shared__ PackDesc sd;
+  const bool first = static_cast<int64_t>(blockIdx.x) < tiles0;
+  static_assert(sizeof(PackDesc) % 4 == 0, "PackDesc copied as words");
+  if (threadIdx.x < sizeof(PackDesc) / 4) {
+    const uint32_t w0 = reinterpret_cast<const uint32_t*>(&d0)[threadIdx.x];
+    const uint32_t w1 = reinterpret_cast<const uint32_t*>(&d1)[threadIdx.x];
+    reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = first ? w0 : w1;
+  }
+  __syncthreads();
+  const PackDesc& d = sd;
+  D* dst = first ? dst0 : dst1;
+  const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
+  auto sync = [] { __syncthreads(); };
+  if (d.side == MDG_SIDE_LEFT) packtile::pack_tile_vec<S, D, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
+  else packtile::pack_tile_vec<S, D, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
 }
 
 // Both operands of a call in one launch when they share source type, target
@@ -71,13 +98,6 @@ __global__ void __launch_bounds__(PACK_THREADS, pack_min_blocks<SRC_COMPLEX>())
   D* dst = first ? dst0 : dst1;
   const int64_t bid = first ? static_cast<int64_t>(blockIdx.x) : static_cast<int64_t>(blockIdx.x) - tiles0;
   auto sync = [] { __syncthreads(); };
-  if constexpr (!SRC_COMPLEX && FMT == MDG_FMT_STANDARD) {
-    if (d.vec) {  // uniform per CTA
-      if (d.side == MDG_SIDE_LEFT) packtile::pack_tile_vec<S, D, MDG_SIDE_LEFT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
-      else packtile::pack_tile_vec<S, D, MDG_SIDE_RIGHT, PACK_THREADS>(d, dst, bid, tile, threadIdx.x, sync);
-      return;
-    }
-  }
   if (d.side == MDG_SIDE_LEFT)
     packtile::pack_tile<S, SRC_COMPLEX, D, FMT, MDG_SIDE_LEFT, PACK_THREADS, packtile::TpcOf<S, SRC_COMPLEX>::value>(d, dst, bid, tile, threadIdx.x, sync);
   else
@@ -169,10 +189,17 @@ PackDesc with_vec(const PackDesc& d, const void* dst) {
 
 template <typename S, bool SC, typename D, int FMT>
 cudaError_t go_pair(const PackDesc& a0, void* da, const PackDesc& b0, void* db, cudaStream_t s) {
-  const PackDesc a = with_vec(a0, da), b = with_vec(b0, db);
+  const PackDesc a = with_vec(a0, da), b = with_vec(b0, db);  // (launch_pack_pair: a.vec == b.vec)
   const int64_t ta = packtile::pack_ctas(a), tb = packtile::pack_ctas(b);
   if (ta + tb == 0) return cudaSuccess;
   if (ta + tb > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  if constexpr (!SC && FMT == MDG_FMT_STANDARD) {
+    if (a.vec) {
+      pack_pair_vec_kernel<S, D><<<static_cast<unsigned>(ta + tb), PACK_THREADS, 0, s>>>(a, static_cast<D*>(da), b,
+                                                                                        static_cast<D*>(db), ta);
+      return cudaGetLastError();
+    }
+  }
   pack_pair_kernel<S, SC, D, FMT><<<static_cast<unsigned>(ta + tb), PACK_THREADS, 0, s>>>(
       a, static_cast<D*>(da), b, static_cast<D*>(db), ta);
   return cudaGetLastError();
@@ -211,6 +238,15 @@ cudaError_t go_side(const PackDesc& d0, void* dst, cudaStream_t s) {
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   const dim3 grid(static_cast<unsigned>(tiles));
+  if constexpr (!SC && FMT == MDG_FMT_STANDARD) {
+    if (d.vec) {
+      if (d.side == MDG_SIDE_LEFT)
+        pack_vec_kernel<S, D, MDG_SIDE_LEFT><<<grid, PACK_THREADS, 0, s>>>(d, static_cast<D*>(dst));
+      else
+        pack_vec_kernel<S, D, MDG_SIDE_RIGHT><<<grid, PACK_THREADS, 0, s>>>(d, static_cast<D*>(dst));
+      return cudaGetLastError();
+    }
+  }
   if (d.side == MDG_SIDE_LEFT)
     pack_kernel<S, SC, D, FMT, MDG_SIDE_LEFT><<<grid, PACK_THREADS, 0, s>>>(d, static_cast<D*>(dst));
   else
@@ -281,7 +317,9 @@ cudaError_t launch_pack_group(PackGroup& g, cudaStream_t s) {
 }
 
 cudaError_t launch_pack_pair(const PackDesc& a, void* da, const PackDesc& b, void* db, cudaStream_t s) {
-  if (a.src.dtype != b.src.dtype || a.target_single != b.target_single || a.format != b.format) {
+  // one kernel for both packs: same source type, target and format, and both or neither on vector tiles
+  if (a.src.dtype != b.src.dtype || a.target_single != b.target_single || a.format != b.format ||
+      with_vec(a, da).vec != with_vec(b, db).vec) {
     const cudaError_t e = launch_pack(a, da, s);
     return e != cudaSuccess ? e : launch_pack(b, db, s);
   }

@@ -145,8 +145,8 @@ __device__ __forceinline__ void put_packed(const PackDesc& d, D* __restrict__ ds
   }
 }
 
-// A scalar tile that lies inside the source (no padding, no edge) of a source with a unit-stride axis,
-// whose 32 panel-axis indices fall into one panel: no bounds tests, one 64-bit tile origin per side and
+// A scalar tile that lies inside the source (no padding, no edge) and whose 32 panel-axis indices fall
+// into one panel: no bounds tests, one 64-bit tile origin per side and
 // 32-bit offsets inside the tile.  (ncu of the c -> s pack pair of a 4096^2 call: ALU pipe 61 % busy, issue
 // slots 65 %, DRAM 35 % -- the packs of 4- and 8-byte elements were bound by their index arithmetic.)
 // Same loads, same element pipeline, same stores as pack_tile's general path.
@@ -160,13 +160,13 @@ __device__ __forceinline__ void pack_tile_interior(const PackDesc& d, D* __restr
   using P = typename Pair<D>::T;
   const int lane = t & 31, row = t >> 5;
   const bool i_fast = d.src.rs <= d.src.cs;
-  const int64_t ld = i_fast ? d.src.cs : d.src.rs;  // the other stride is 1
+  const int64_t sc = i_fast ? d.src.rs : d.src.cs, sl = i_fast ? d.src.cs : d.src.rs;  // strides along the lanes / the lines
   const S* sp = reinterpret_cast<const S*>(d.src.base) + (ti0 * d.src.rs + tj0 * d.src.cs) * NC;
   const bool cvec = d.cvec != 0;
   Raw<S, SRC_COMPLEX> raw[PER];
 #pragma unroll
   for (int r = 0; r < PER; ++r) {
-    const S* p = sp + (lane + (row + ROWS * r) * ld) * NC;
+    const S* p = sp + (lane * sc + (row + ROWS * r) * sl) * NC;
     if constexpr (SRC_COMPLEX) {
       if (cvec) {
         using V = typename std::conditional<sizeof(S) == 4, float2, double2>::type;
@@ -230,10 +230,10 @@ __device__ __forceinline__ void pack_tile(const PackDesc& d, D* __restrict__ dst
   constexpr int PER = TILE / ROWS;
   const int64_t tiles_i = (d.ext_i + TILE - 1) / TILE;
   const int64_t tiles = tiles_i * ((d.ext_j + TILE - 1) / TILE);
-  if constexpr (TPC == 1 && SRC_COMPLEX) {  // (real sources with a unit-stride axis take the vector tiles)
+  if constexpr (TPC == 1) {
     constexpr int FX = FMT == MDG_FMT_ONEE ? 2 : 1;
     const int64_t ti0 = (bid % tiles_i) * TILE, tj0 = (bid / tiles_i) * TILE;
-    if (bid < tiles && (d.src.rs <= d.src.cs ? d.src.rs == 1 : d.src.cs == 1) && ti0 + TILE <= d.src.m && tj0 + TILE <= d.src.n &&
+    if (bid < tiles && ti0 + TILE <= d.src.m && tj0 + TILE <= d.src.n &&
         d.pd_shift >= 5 + (FX == 2 ? 1 : 0) && d.interior) {  // uniform per CTA
       pack_tile_interior<S, SRC_COMPLEX, D, FMT, SIDE, NT>(d, dst, ti0, tj0, tile, t, sync);
       return;

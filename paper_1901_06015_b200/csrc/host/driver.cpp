@@ -786,16 +786,19 @@ void dual_pack_group(mdg::PackGroup& g, double traffic, cudaStream_t st) {
 }
 
 int dual_grid() {
-  // Two SMs are left to the next launches' pack kernels: a dual CTA holds
+  // One SM is left to the next launches' pack kernels: a dual CTA holds
   // every register of its SM, so without them those packs wait for the launch
   // to drain and the kernel stream idles while they run.  Measured on the cfg2
   // sweep (profiles/r02/dual_spare_sms.txt): 0 spare SMs -> 52,470 GFLOPS,
   // 1 -> 52,640, 2 -> 52,620, 4 -> 52,390 with two pack arenas; 2 spare SMs
   // with three arenas (staging.cpp: dual_arenas, the packs may run two
-  // launches ahead) -> 52,710.  MDGEMM_DUAL_SPARE_SMS overrides.
+  // launches ahead) -> 52,710.  With the faster packs of the end of round 2
+  // (vector / interior tiles) one spare SM is enough: 0 -> 53,280, 1 -> 53,520,
+  // 2 -> 53,420, 3 -> 53,130 (profiles/r02/dual_spare_sms_vec.txt).
+  // MDGEMM_DUAL_SPARE_SMS overrides.
   static const int spare = [] {
     const char* f = std::getenv("MDGEMM_DUAL_SPARE_SMS");
-    return f ? std::max(0, std::atoi(f)) : 2;
+    return f ? std::max(0, std::atoi(f)) : 1;
   }();
   int dev_count = 0;
   const int sms = cudaGetDeviceCount(&dev_count) == cudaSuccess && dev_count > 0 ? device_sms() : 148;

@@ -44,4 +44,5 @@ done
 ncu -i $O/prof_dual.ncu-rep --page source --csv --print-source sass > $O/ncu_dual_source.csv 2>/dev/null
 python tools/ncu_stalls.py $O/ncu_dual_source.csv > $O/dual_stalls.txt 2>&1
 rm -f $O/ncu_dual_source.csv
+rm -f $O/*.ncu-rep   # gpurun brings back at most 64 MiB: the CSV exports are what profiles/ keeps
 echo done
