@@ -4,10 +4,15 @@
 //   v = widen(src) -> conj (src.conj xor requested) -> round to the target
 //   precision -> if scale != 1: complex<double> product, round again.
 //
-// Data movement: one CTA stages a 32x32 source tile in shared memory, read
-// coalesced along the source's unit-stride axis and written coalesced along
-// the packed buffer's contiguous axis (rows for left panels, columns for
-// right panels), so a transposing pack costs one HBM read and one HBM write.
+// Data movement (pack_tile.cuh): one CTA moves one source tile -- 32x32
+// elements, or 32 lines of 16-byte vectors for real sources with a
+// unit-stride axis and aligned lines -- read coalesced along the source's
+// unit-stride axis and written coalesced along the packed buffer's contiguous
+// axis (rows for left panels, columns for right panels), through shared memory
+// when the two differ, so a transposing pack costs one HBM read and one HBM
+// write.  The launchers pick the kernel: pack_kernel / pack_vec_kernel for one
+// operand, pack_pair_kernel / pack_pair_vec_kernel for both operands of a call,
+// pack_group_kernel for the many small packs of a dual launch.
 #include <cstdlib>
 #include <type_traits>
 

@@ -1,11 +1,21 @@
-// One 32x32 source tile of a typecasting pack (Standard / 1e / 1r, left or
-// right panels, conjugation, alpha scaling) -- the body of pack.cu's kernels.  Bit-exact against the
-// reference pack (packing.cpp:114-230):
+// The tiles of a typecasting pack (Standard / 1e / 1r, left or right panels,
+// conjugation, alpha scaling) -- the bodies of pack.cu's kernels.  Bit-exact
+// against the reference pack (packing.cpp:114-230):
 //   v = widen(src) -> conj (src.conj xor requested) -> round to the target
 //   precision -> if scale != 1: complex<double> product, round again.
-// The tile moves through shared memory, read coalesced along the source's
-// unit-stride axis and written coalesced along the packed panels' contiguous
-// axis.
+// Three bodies share that element pipeline (process_typed) and the panel
+// layout (put_packed's offsets), so their packed bytes are identical:
+//   pack_tile           a 32x32 source tile, any strides, any extents (bounds
+//                       tests, padding, 64-bit index arithmetic);
+//   pack_tile_interior  the same tile when it lies inside the source and its
+//                       panel-axis indices share a panel: no tests, 32-bit
+//                       offsets from one 64-bit origin per side;
+//   pack_tile_vec       real sources with a unit-stride axis and 16-byte
+//                       aligned lines: 32 lines x 32 V elements in 8- / 16-byte
+//                       vectors.
+// A tile is read coalesced along the source's unit-stride axis and written
+// coalesced along the packed panels' contiguous axis, through shared memory
+// when the two differ.
 #pragma once
 
 #include <type_traits>
